@@ -1,0 +1,381 @@
+"""Benchmark: MLS-MPM Neo-Hookean substep throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3] [--particles P] [--no-cpu-baseline]
+
+Workload (N=1): BASELINE config 3 -- a 1 M-particle Neo-Hookean slab on a
+256^3 grid pressed by a box tool moving down at 0.5 m/s (SimParams defaults:
+dt 5e-4, 25 substeps per step, theta 0.5 dx, Coulomb mu 0.4).  One "step" is
+one ``softmpm.step`` frame = 25 substeps.  Metric: particle-substeps/s.
+
+* value     device-resident frames timed with CUDA events on the context
+            stream (pose table built on the host and uploaded per frame, as
+            ``step`` does); L2 is flushed (512 MiB memset) between frames.
+* e2e       same frames through the C-ABI with HOST fp64 buffers: upload of
+            x/v/F/C from pinned memory + 25 substeps + download of x/v/F/C,
+            wall clock with the copies inside the timed region.
+* roofline  dominant kernel = fused_kernel (one launch = one substep of every
+            particle); achieved = 200 B x particles / mean launch time
+            (SURVEY §8d), peak = MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline  the CPU oracle O1 (oracle/, C restatement of the reference's
+            numba kernels, OpenMP over all host cores) on a bounded sample of
+            the same scene.
+* --impl reference  times that CPU path alone on this config (the driver's
+            reference arm); rank 0 only under torchrun.
+N>1 (torchrun): every rank runs its own replica scene on its own GPU (batched
+independent environments, BASELINE config 4 style; no data-path
+collective) -> "scaling": "weak"; time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-substeps/sec (MLS-MPM, Neo-Hookean)"
+UNIT = "particle-substeps/s"
+BYTES_PER_PARTICLE_SUBSTEP = 200  # fp32 x,v,F,C read+written once + mass,vol0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_scene(config: str, particles: int | None, seed: int):
+    from paper_2402_01181_b200 import scenes
+    kw = {"seed": seed}
+    if particles:
+        kw["count"] = particles
+    return scenes.BUILDERS[config](**kw)
+
+
+def pose_rows(st, cols, params, pose_fn, t0):
+    """Per-substep pose table exactly as core.step builds it."""
+    R, T, lv, av, md = [], [], [], [], []
+    t = t0
+    for _ in range(params.substeps_per_frame):
+        pose_fn(cols, t)
+        pk = st._packed_colliders(cols, params)
+        R.append(pk.rotation.copy())
+        T.append(pk.translation.copy())
+        lv.append(pk.linear_velocity.copy())
+        av.append(pk.angular_velocity.copy())
+        md.append(pk.mode.copy())
+        t += params.dt
+    return [np.ascontiguousarray(a) for a in (R, T, lv, av)] + [np.ascontiguousarray(md, np.int32)]
+
+
+def cpu_oracle_rate(config, particles, seed, substeps, threads):
+    """O1 (fp64 CPU restatement of the reference kernels) particle-substeps/s."""
+    from oracle import oracle as O
+    import paper_2402_01181_b200 as sm
+    st, mats, params, cols, pose_fn = build_scene(config, particles, seed)
+    O.set_threads(threads)
+    g = st.grid
+    op = O.OracleParams(res=g.resolution, dx=g.dx, theta=0.5 * g.dx, chunks=8)
+    osim = O.OracleSim(op, st.x, st.v, st.F, st.C, st.mass, st.vol0, st.material_id, mats[0].mu,
+                       mats[0].lam)
+    t = 0.0
+    times = []
+    for i in range(substeps + 1):
+        t0 = time.perf_counter()
+        if cols:
+            pose_fn(cols, t)
+        osim.substep(sm.pack_colliders(cols) if cols else None)
+        times.append(time.perf_counter() - t0)
+        t += params.dt
+    n = st.particle_count
+    dt_med = float(np.median(times[1:]))
+    return n / dt_med, times[1:], n
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    import paper_2402_01181_b200 as sm
+    st, mats, params, cols, pose_fn = build_scene(args.config, args.particles, 1)
+    g = st.grid
+    op = O.OracleParams(res=g.resolution, dx=g.dx, theta=0.5 * g.dx, chunks=8)
+    osim = O.OracleSim(op, st.x, st.v, st.F, st.C, st.mass, st.vol0, st.material_id, mats[0].mu,
+                       mats[0].lam)
+    n = st.particle_count
+    t = 0.0
+    per = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if cols:
+            pose_fn(cols, t)
+        osim.substep(sm.pack_colliders(cols) if cols else None)
+        el = time.perf_counter() - t0
+        t += params.dt
+        if i >= args.warmup:
+            per.append(el)
+    tot = sum(per)
+    value = n * len(per) / tot
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / len(per),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {n} particles, {g.resolution[0]}^3 grid, "
+                   f"{len(cols)} tool(s)", "particles": n, "grid": list(g.resolution)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"each step = 1 substep of the full {args.config} scene "
+                                   f"(O1 fp64 C restatement of kernels.py, 8 chunks, OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import paper_2402_01181_b200 as sm
+    from paper_2402_01181_b200 import _lib
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    st, mats, params, cols, pose_fn = build_scene(args.config, args.particles, 1 + rank)
+    st.device = local_rank
+    n = st.particle_count
+    nsub = params.substeps_per_frame
+    L = _lib.lib()
+
+    # warm-up through the public API (creates the context, uploads, JITs nothing)
+    for _ in range(args.warmup):
+        sm.step(st, mats, params, cols, pose_fn)
+    ctx = st._ctx
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
+
+    def frame():
+        rows = pose_rows(st, cols, params, pose_fn, st.time) if cols else None
+        if cols:
+            st._upload_pose_rows(*rows)
+        inv = ctypes.c_int64(0)
+        ms = ctypes.c_double(0.0)
+        ctx.call("mpm_substeps", nsub, int(bool(cols)), ctypes.byref(inv), ctypes.byref(ms))
+        for _ in range(nsub):
+            st.time += params.dt
+        st._device_wrote(("x", "v", "F", "C"))
+        return ms.value
+
+    # ---- device-resident timed region ------------------------------------
+    L.mpm_set_timing(ctx.h, 1)
+    launches0 = ctx.launches
+    dev_ms = 0.0
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dev_ms += frame()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if dist:
+        tdist.barrier()
+    launches = ctx.launches - launches0
+    tbuf = (ctypes.c_double * 10)()
+    L.mpm_get_timing(ctx.h, tbuf)
+    L.mpm_set_timing(ctx.h, 0)
+    fused_ms, fused_n = tbuf[0], max(tbuf[1], 1.0)
+    grid_ms, grid_n = tbuf[2], max(tbuf[3], 1.0)
+    rebin_ms, g2p_ms = tbuf[4], tbuf[6]
+    t_dev = dev_ms / 1000.0
+    if dist:
+        tt = torch.tensor([t_dev], device=f"cuda:{local_rank}", dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    total_units = n * world * nsub * args.steps
+    value = total_units / t_dev
+
+    # ---- e2e through the C-ABI with host buffers ---------------------------
+    e2e_steps = max(2, args.steps // 2)
+    host = {}
+    sizes = {"x": 3, "v": 3, "F": 9, "C": 9}
+    ptrs = []
+    for k, w in sizes.items():
+        nbytes = n * w * 8
+        p = L.mpm_host_alloc(nbytes)
+        if not p:
+            host[k] = np.empty(n * w)
+        else:
+            ptrs.append(p)
+            host[k] = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)),
+                                            shape=(n * w,))
+    ctx.call("mpm_download_particles", ctypes.c_uint32(15), *[_lib.ptr(host[k]) for k in sizes])
+    h2d = d2h = n * 24 * 8
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.call("mpm_upload_fields", ctypes.c_uint32(15), *[_lib.ptr(host[k]) for k in sizes])
+        frame()
+        ctx.call("mpm_download_particles", ctypes.c_uint32(15), *[_lib.ptr(host[k]) for k in sizes])
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - e0
+    if dist:
+        tt = torch.tensor([t_e2e], device=f"cuda:{local_rank}", dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = n * world * nsub * e2e_steps / t_e2e
+    for p in ptrs:
+        L.mpm_host_free(p)
+    assert not st.has_nan(), "simulation produced NaN"
+
+    if rank != 0:
+        return
+    peak, peak_src = _peaks()
+    avg_fused_s = fused_ms / fused_n / 1000.0
+    achieved = BYTES_PER_PARTICLE_SUBSTEP * n / avg_fused_s / 1e9
+    substep_s = t_dev / (args.steps * nsub)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {n} particles/GPU, {st.grid.resolution[0]}^3 grid, "
+                   f"{len(cols)} box tool(s) pressing at 0.5 m/s, 25 substeps per step",
+                   "particles_per_gpu": n, "grid": list(st.grid.resolution),
+                   "substeps_per_step": nsub, "parallelism": f"replicas x{world}",
+                   "l2": "flushed between steps (512 MiB memset)",
+                   "wall_s_timed": wall},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "fused_kernel (G2P+advect+F+stress+P2G, one launch = 1 substep)",
+                     "bytes_per_launch": BYTES_PER_PARTICLE_SUBSTEP * n,
+                     "mean_launch_ms": 1000.0 * avg_fused_s, "peak_source": peak_src,
+                     "substep_frac": (BYTES_PER_PARTICLE_SUBSTEP * n / substep_s / 1e9) / peak,
+                     "share_of_step": fused_ms / max(dev_ms, 1e-9)},
+        "kernel_ms": {"fused_mean": fused_ms / fused_n, "grid_op_mean": grid_ms / grid_n,
+                      "rebin_total": rebin_ms, "g2p_total": g2p_ms, "device_total": dev_ms,
+                      "active_bricks": tbuf[8], "work_items": tbuf[9]},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, times, nn = cpu_oracle_rate(args.config, args.particles, 1, args.cpu_substeps, threads)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                               "sample": f"{args.cpu_substeps} substeps (after 1 warm-up) of the "
+                                         f"same {args.config} scene, {nn} particles, O1 fp64 C "
+                                         f"restatement of kernels.py, 8 chunks, OpenMP",
+                               "substep_s": times}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--particles", type=int, default=None)
+    ap.add_argument("--cpu-substeps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3 if args.impl == "ours" else args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * softmpm_b200.h -- C ABI of the B200-native MLS-MPM substep.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * package (softmpm, /root/reference/pkg/src/softmpm) has no native ABI: its
+ * "operator ABI" is the set of numba kernels called by core.py with flat
+ * numpy arrays.  Each entry point below names the reference interface it
+ * replaces.  Conventions:
+ *   - every function returns 0 on success, a negative MPM_E* code otherwise;
+ *     mpm_last_error(ctx) holds the message;
+ *   - host arrays are the reference's fp64 C-order numpy layouts
+ *     (x/v (n,3), F/C (n,3,3) row-major, grid_mv (nx,ny,nz,3), grid_m
+ *     (nx,ny,nz)); they are borrowed for the duration of the call only;
+ *   - particle order on the host is always the caller's original order; the
+ *     device keeps its own binned permutation;
+ *   - calls are synchronous with respect to the host buffers passed in and
+ *     may be made from any host thread (each call sets the device itself).
+ */
+#ifndef SOFTMPM_B200_H
+#define SOFTMPM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPM_OK 0
+#define MPM_EINVAL -1   /* invalid argument -> softmpm.errors.ParameterError */
+#define MPM_ENOMEM -2   /* device/host allocation failed -> SimError */
+#define MPM_ECUDA -3    /* CUDA runtime error -> SimError */
+#define MPM_ESTATE -4   /* call out of order (e.g. no particles) -> SimError */
+#define MPM_ESTENCIL -5 /* particle outside the 1.5-cell margin -> StencilError */
+
+/* field masks for upload/download */
+#define MPM_FIELD_X 1u
+#define MPM_FIELD_V 2u
+#define MPM_FIELD_F 4u
+#define MPM_FIELD_C 8u
+#define MPM_FIELD_ALL 15u
+
+/* stress forms */
+#define MPM_STRESS_KERNEL 0 /* P = mu F + ((lam lnJ - mu)/J) cof^T : kernels.py:253-262 */
+#define MPM_STRESS_SPEC 1   /* P = mu (F - F^-T) + lam lnJ F^-T  : materials.py:59-60  */
+
+typedef struct mpm_ctx mpm_ctx;
+
+/* Mirrors Grid (core.py:24-56) + SimParams (core.py:59-79) + build options. */
+typedef struct {
+  int device;
+  int res[3];           /* Grid.resolution */
+  double dx;            /* Grid.dx (uniform) */
+  double dt;            /* SimParams.dt */
+  double gravity[3];    /* SimParams.gravity */
+  int boundary_width;   /* SimParams.boundary_width */
+  int stick;            /* SimParams.boundary == "stick" */
+  double theta;         /* collision band; < 0 disables (core.py:290-291) */
+  int stress_form;      /* MPM_STRESS_* */
+  int mode_live;        /* 0: collider mode frozen at first pack (F7 compat), 1: live */
+  int deterministic;    /* 1: sorted deterministic-order P2G (bit-exact grid mass) */
+  int rebin_interval;   /* substeps between particle re-binning (fast mode), >= 1 */
+} mpm_config;
+
+/* ---- lifetime ---------------------------------------------------------- */
+int mpm_create(mpm_ctx **out, const mpm_config *cfg);
+int mpm_destroy(mpm_ctx *ctx);
+/* Replace dt/gravity/boundary/theta/stress options (SimParams changes between calls). */
+int mpm_set_config(mpm_ctx *ctx, const mpm_config *cfg);
+const char *mpm_last_error(mpm_ctx *ctx);
+const char *mpm_version(void);
+
+/* ---- materials: replaces materials.pack_materials (materials.py:77-82) --- */
+int mpm_set_materials(mpm_ctx *ctx, const double *mu, const double *lam, int count);
+
+/* ---- particle state: SimState x/v/F/C/mass/vol0/material_id (core.py:92-143) */
+int mpm_upload_particles(mpm_ctx *ctx, int64_t n, const double *x, const double *v,
+                         const double *F, const double *C, const double *mass,
+                         const double *vol0, const int32_t *material_id);
+/* Overwrite a subset of x/v/F/C (host-side edits of SimState fields). */
+int mpm_upload_fields(mpm_ctx *ctx, uint32_t mask, const double *x, const double *v,
+                      const double *F, const double *C);
+int mpm_download_particles(mpm_ctx *ctx, uint32_t mask, double *x, double *v, double *F,
+                           double *C);
+int64_t mpm_particle_count(mpm_ctx *ctx);
+
+/* ---- grid: SimState.grid_mv / grid_m (core.py:106-117) ------------------ */
+/* target 0: the momentum buffer read by grid_update, 1: the velocity buffer
+ * read by g2p_advect.  grid_m may be NULL (target 1). */
+int mpm_upload_grid(mpm_ctx *ctx, int target, const double *grid_mv, const double *grid_m);
+/* Download grid_mv as SimState shows it after the last stage, and grid_m. */
+int mpm_download_grid(mpm_ctx *ctx, double *grid_mv, double *grid_m);
+
+/* ---- colliders: replaces collision.pack_colliders / PackedColliders
+ *      (collision.py:174-241).  Geometry is static; poses change per substep. */
+int mpm_set_colliders(mpm_ctx *ctx, int count, const int32_t *kind, const double *half,
+                      const double *rotation, const double *translation,
+                      const double *linear_velocity, const double *angular_velocity,
+                      const double *friction, const int32_t *mode, const double *sdf_values,
+                      int64_t sdf_len, const int64_t *sdf_offset, const int32_t *sdf_resolution,
+                      const double *sdf_bounds_min, const double *sdf_extent);
+/* Pose table for the next `nsub` substeps (PackedColliders.refresh_poses per
+ * substep, collision.py:192-197); arrays are (nsub, count, ...).  mode may be
+ * NULL (keep the packed/frozen mode). */
+int mpm_set_pose_table(mpm_ctx *ctx, int nsub, const double *rotation,
+                       const double *translation, const double *linear_velocity,
+                       const double *angular_velocity, const int32_t *mode);
+
+/* ---- stage operators (core.py:211-258; kernels.py:198-534) --------------- */
+/* p2g_scatter + p2g_reduce: F advanced in place; *inverted = det<=0 count. */
+int mpm_p2g(mpm_ctx *ctx, int64_t *inverted);
+/* kernels.grid_update with the collision field of build_collision_field
+ * evaluated lazily at massive nodes; use_colliders selects pose row 0. */
+int mpm_grid_update(mpm_ctx *ctx, int use_colliders);
+/* kernels.g2p_advect */
+int mpm_g2p(mpm_ctx *ctx);
+
+/* ---- fused driver: core.substep x nsub (core.py:261-320) ---------------- */
+/* Runs nsub substeps device-resident; colliders use pose row s at substep s
+ * when use_colliders.  *inverted = summed det<=0 count; stage_ms (may be
+ * NULL) receives device milliseconds of the whole sequence. */
+int mpm_substeps(mpm_ctx *ctx, int nsub, int use_colliders, int64_t *inverted,
+                 double *device_ms);
+
+/* ---- diagnostics -------------------------------------------------------- */
+/* update_collision_field (collision.py:244-272) over all nodes, current pose
+ * row 0; dist (nx,ny,nz) f64, obj (nx,ny,nz) i32, cap = 2 theta. */
+int mpm_collision_field(mpm_ctx *ctx, double theta, double *dist, int32_t *obj);
+/* SimState.has_nan (core.py:149-151) on device. */
+int mpm_has_nan(mpm_ctx *ctx, int *flag);
+/* Per-kernel CUDA-event timing on the context stream (bench/roofline).
+ * When enabled every fast-path launch is bracketed by events; mpm_get_timing
+ * fills out[10] = {fused_ms, fused_launches, grid_op_ms, grid_op_launches,
+ * rebin_ms, rebin_calls, g2p_ms, g2p_launches, active_bricks_last,
+ * work_items_last} accumulated since the last enable, and resets them. */
+int mpm_set_timing(mpm_ctx *ctx, int enable);
+int mpm_get_timing(mpm_ctx *ctx, double *out);
+/* Kernel launches issued by this context so far (evidence counter). */
+int64_t mpm_launch_count(mpm_ctx *ctx);
+/* Page-locked host buffer for fast uploads/downloads (e2e path). */
+void *mpm_host_alloc(int64_t bytes);
+void mpm_host_free(void *ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOFTMPM_B200_H */

@@ -1,0 +1,200 @@
+// collide.cuh -- rigid-tool geometry and contact response on the device.
+//
+// fp64 with every product/sum explicitly rounded (no FMA contraction) so the
+// merged distance field and contact normals equal the reference's numba
+// kernels bit for bit (kernels.py:30-191, fastmath off):
+//   box_sd      <- _box_signed_distance      kernels.py:30-45
+//   baked_sd    <- _sample_baked             kernels.py:48-88
+//   world_sd    <- _collider_world_distance  kernels.py:102-113
+//   world_normal<- _collider_world_normal    kernels.py:116-158
+//   resolve     <- grid_update contact block kernels.py:371-411
+// Only massive nodes inside the band evaluate these (the reference rebuilds
+// the field over every node, kernels.py:161-191; the result at consumed nodes
+// is identical).
+#pragma once
+#include <cstdint>
+
+namespace mpm {
+
+constexpr int MAX_COLLIDERS = 16;
+
+struct ColliderGeo {
+  int kind;  // 0 box, 1 baked
+  double half[3];
+  double fric;
+  int mode;  // packed (frozen) mode
+  long long sdf_off;
+  int sdf_res[3];
+  double sdf_bmin[3];
+  double sdf_ext;
+};
+
+struct ColliderPose {
+  double R[9];
+  double T[3];
+  double lv[3];
+  double av[3];
+  int mode;
+};
+
+struct Colliders {
+  int count;
+  double theta;  // < 0: disabled
+  const ColliderGeo* geo;
+  const ColliderPose* pose;  // row for this substep
+  const double* sdf;
+};
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ inline double box_sd(double px, double py, double pz, const double h[3]) {
+  double qx = ds(fabs(px), h[0]), qy = ds(fabs(py), h[1]), qz = ds(fabs(pz), h[2]);
+  double ox = qx > 0.0 ? qx : 0.0, oy = qy > 0.0 ? qy : 0.0, oz = qz > 0.0 ? qz : 0.0;
+  double outside = __dsqrt_rn(da(da(dm(ox, ox), dm(oy, oy)), dm(oz, oz)));
+  double qm = qx;
+  if (qy > qm) qm = qy;
+  if (qz > qm) qm = qz;
+  return da(outside, qm < 0.0 ? qm : 0.0);
+}
+
+__device__ inline double baked_sd(const ColliderGeo& g, const double* sdf, double px, double py,
+                                  double pz) {
+  const double p[3] = {px, py, pz};
+  long long i0[3];
+  double fr[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double r = (double)g.sdf_res[a];
+    double c = ds(dm(__ddiv_rn(ds(p[a], g.sdf_bmin[a]), g.sdf_ext), r), 0.5);
+    if (c < 0.0) c = 0.0;
+    if (c > r - 1.0) c = r - 1.0;
+    long long ii = (long long)c;
+    if (ii > g.sdf_res[a] - 2) ii = g.sdf_res[a] - 2;
+    i0[a] = ii;
+    fr[a] = ds(c, (double)ii);
+  }
+  const double* v = sdf + g.sdf_off;
+  long long rx = g.sdf_res[0], ry = g.sdf_res[1];
+  double s = 0.0;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    double wa = a ? fr[0] : ds(1.0, fr[0]);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      double wb = b ? fr[1] : ds(1.0, fr[1]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double wc = c ? fr[2] : ds(1.0, fr[2]);
+        long long idx = (i0[0] + a) + rx * ((i0[1] + b) + ry * (i0[2] + c));
+        s = da(s, dm(dm(dm(wa, wb), wc), __ldg(v + idx)));
+      }
+    }
+  }
+  return dm(s, g.sdf_ext);
+}
+
+__device__ inline double local_sd(const ColliderGeo& g, const double* sdf, double px, double py,
+                                  double pz) {
+  if (g.kind == 0) return box_sd(px, py, pz, g.half);
+  return baked_sd(g, sdf, px, py, pz);
+}
+
+__device__ inline void to_local(const ColliderPose& q, double wx, double wy, double wz,
+                                double& px, double& py, double& pz) {
+  double d0 = ds(wx, q.T[0]), d1 = ds(wy, q.T[1]), d2 = ds(wz, q.T[2]);
+  px = da(da(dm(q.R[0], d0), dm(q.R[3], d1)), dm(q.R[6], d2));
+  py = da(da(dm(q.R[1], d0), dm(q.R[4], d1)), dm(q.R[7], d2));
+  pz = da(da(dm(q.R[2], d0), dm(q.R[5], d1)), dm(q.R[8], d2));
+}
+
+__device__ inline double world_sd(const Colliders& cs, int ci, double wx, double wy, double wz) {
+  double px, py, pz;
+  to_local(cs.pose[ci], wx, wy, wz, px, py, pz);
+  return local_sd(cs.geo[ci], cs.sdf, px, py, pz);
+}
+
+// Merged field at one node: min distance, ties to the lowest index, id -1
+// beyond cap = 2 theta (kernels.py:180-191).
+__device__ inline int nearest_collider(const Colliders& cs, double wx, double wy, double wz,
+                                       double cap, double& best) {
+  best = 1.0e30;
+  int id = -1;
+  for (int ci = 0; ci < cs.count; ++ci) {
+    double d = world_sd(cs, ci, wx, wy, wz);
+    if (d < best) {
+      best = d;
+      id = ci;
+    }
+  }
+  return best >= cap ? -1 : id;
+}
+
+__device__ inline void world_normal(const Colliders& cs, int ci, double wx, double wy, double wz,
+                                    double n[3]) {
+  const ColliderGeo& g = cs.geo[ci];
+  const ColliderPose& q = cs.pose[ci];
+  double px, py, pz;
+  to_local(q, wx, wy, wz, px, py, pz);
+  double h;
+  if (g.kind == 0) {
+    h = g.half[0];
+    if (g.half[1] < h) h = g.half[1];
+    if (g.half[2] < h) h = g.half[2];
+    h = dm(1.0e-3, h);
+    if (h < 1.0e-6) h = 1.0e-6;
+  } else {
+    h = __ddiv_rn(g.sdf_ext, (double)g.sdf_res[0]);
+  }
+  double gx = ds(local_sd(g, cs.sdf, da(px, h), py, pz), local_sd(g, cs.sdf, ds(px, h), py, pz));
+  double gy = ds(local_sd(g, cs.sdf, px, da(py, h), pz), local_sd(g, cs.sdf, px, ds(py, h), pz));
+  double gz = ds(local_sd(g, cs.sdf, px, py, da(pz, h)), local_sd(g, cs.sdf, px, py, ds(pz, h)));
+  double norm = __dsqrt_rn(da(da(dm(gx, gx), dm(gy, gy)), dm(gz, gz)));
+  if (norm < 1.0e-12) {
+    double fx = ds(wx, q.T[0]), fy = ds(wy, q.T[1]), fz = ds(wz, q.T[2]);
+    double fn = __dsqrt_rn(da(da(dm(fx, fx), dm(fy, fy)), dm(fz, fz)));
+    if (fn < 1.0e-12) {
+      n[0] = 0.0; n[1] = 1.0; n[2] = 0.0;
+      return;
+    }
+    n[0] = __ddiv_rn(fx, fn); n[1] = __ddiv_rn(fy, fn); n[2] = __ddiv_rn(fz, fn);
+    return;
+  }
+  gx = __ddiv_rn(gx, norm); gy = __ddiv_rn(gy, norm); gz = __ddiv_rn(gz, norm);
+  n[0] = da(da(dm(q.R[0], gx), dm(q.R[1], gy)), dm(q.R[2], gz));
+  n[1] = da(da(dm(q.R[3], gx), dm(q.R[4], gy)), dm(q.R[5], gz));
+  n[2] = da(da(dm(q.R[6], gx), dm(q.R[7], gy)), dm(q.R[8], gz));
+}
+
+// Contact response at a massive node inside the band (kernels.py:371-411).
+__device__ inline void resolve_contact(const Colliders& cs, int ci, double wx, double wy, double wz,
+                                       double v[3]) {
+  const ColliderPose& q = cs.pose[ci];
+  double rx = ds(wx, q.T[0]), ry = ds(wy, q.T[1]), rz = ds(wz, q.T[2]);
+  double co0 = ds(da(q.lv[0], dm(q.av[1], rz)), dm(q.av[2], ry));
+  double co1 = ds(da(q.lv[1], dm(q.av[2], rx)), dm(q.av[0], rz));
+  double co2 = ds(da(q.lv[2], dm(q.av[0], ry)), dm(q.av[1], rx));
+  double r0 = ds(v[0], co0), r1 = ds(v[1], co1), r2 = ds(v[2], co2);
+  double n[3];
+  world_normal(cs, ci, wx, wy, wz, n);
+  double vn = da(da(dm(r0, n[0]), dm(r1, n[1])), dm(r2, n[2]));
+  if (!(vn < 0.0)) return;
+  if (q.mode == 1) {
+    v[0] = co0; v[1] = co1; v[2] = co2;
+    return;
+  }
+  double t0 = ds(r0, dm(vn, n[0])), t1 = ds(r1, dm(vn, n[1])), t2 = ds(r2, dm(vn, n[2]));
+  double tn = __dsqrt_rn(da(da(dm(t0, t0), dm(t1, t1)), dm(t2, t2)));
+  double muf = cs.geo[ci].fric;
+  if (tn <= dm(muf, -vn)) {
+    v[0] = co0; v[1] = co1; v[2] = co2;
+  } else {
+    double scale = da(1.0, __ddiv_rn(dm(muf, vn), tn));
+    v[0] = da(dm(t0, scale), co0);
+    v[1] = da(dm(t1, scale), co1);
+    v[2] = da(dm(t2, scale), co2);
+  }
+}
+
+}  // namespace mpm

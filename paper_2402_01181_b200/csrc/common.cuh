@@ -1,0 +1,223 @@
+// common.cuh -- layouts, launch parameters and stencil math shared by the
+// B200 MLS-MPM kernels.
+//
+// HBM layout:
+//   * particles: SoA fp32, NF float fields of `cap` entries each (x0..2,
+//     v0..2, F00..F22, C00..C22, mass, vol0) + int32 material id + int32
+//     original index, double-buffered so re-binning is a gather-free scatter;
+//     the device order is "grouped by 8^3-cell bin", the host order is the
+//     caller's.
+//   * grid: blocked-dense float4 arrays, 4^3-node bricks of 1 KiB each
+//     (node (i,j,k) -> brick ((i>>2,j>>2,k>>2)) * 64 + local (i&3,j&3,k&3)),
+//     `gm` = (momentum xyz, mass) accumulated by P2G, `gv` = velocity
+//     written by the grid op and read by G2P.  Only bricks touched by P2G
+//     (the active list) are visited by the grid op.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mpm {
+
+constexpr int BRICK_SHIFT = 2;            // 4^3 nodes per layout brick
+constexpr int BRICK_NODES = 64;
+constexpr int BIN = 8;                    // particle bin edge (cells)
+constexpr int BIN_SHIFT = 3;
+constexpr int MARGIN = 2;                 // tile margin for particles drifting out of their bin
+constexpr int TILE = BIN + 2 + 2 * MARGIN;  // 14 nodes per tile edge
+constexpr int TILE_NODES = TILE * TILE * TILE;
+constexpr int CHUNK = 2048;               // max particles per work item
+constexpr int NF = 26;                    // float fields per particle
+
+enum Field : int { FX = 0, FV = 3, FF = 6, FC = 15, FMASS = 24, FVOL = 25 };
+
+struct Params {
+  // grid
+  int res[3];      // node resolution
+  int nb[3];       // layout bricks per axis
+  int nbin[3];     // particle bins per axis
+  float dx, inv_dx, dt;
+  float gravity[3];
+  float lo, hi[3];  // particle margin clamp (core.py:51-56)
+  float stress_coef;  // -4 dt / dx^2 (kernels.py:207)
+  float apic_coef;    // 4 / dx^2 (kernels.py:448)
+  double dx64, dt64;
+  int bwidth, stick, stress_form;
+  // grid buffers
+  float4* gm;
+  float4* gv;
+  int* brick_flag;
+  int* active_list;
+  int* active_count;
+  // particles
+  float* P;
+  int* mat;
+  int* orig;
+  long long cap;
+  long long n;
+  const float* mu;
+  const float* lam;
+  unsigned long long* inverted;
+  // work items (bin, start, end, 0)
+  const int4* work;
+  const int* nwork;
+};
+
+__host__ __device__ inline long long node_index(int i, int j, int k, int nby, int nbz) {
+  long long b = ((long long)(i >> BRICK_SHIFT) * nby + (j >> BRICK_SHIFT)) * nbz + (k >> BRICK_SHIFT);
+  return (b << 6) | ((i & 3) << 4) | ((j & 3) << 2) | (k & 3);
+}
+
+__device__ inline void brick_coords(long long b, const int nb[3], int& bi, int& bj, int& bk) {
+  bk = (int)(b % nb[2]);
+  long long t = b / nb[2];
+  bj = (int)(t % nb[1]);
+  bi = (int)(t / nb[1]);
+}
+
+// Quadratic B-spline stencil of one coordinate (kernels.py:277-294), fp32,
+// base clamped to [0, r-3] (fp32 rounding can push x/dx past the fp64
+// margin of core.py:55; the clamp keeps the 3-node stencil in the grid).
+__device__ __forceinline__ void stencil(float xc, float inv_dx, int r, int& b, float& f,
+                                        float w[3]) {
+  float g = xc * inv_dx;
+  int bb = (int)floorf(g - 0.5f);
+  bb = max(0, min(bb, r - 3));
+  f = g - (float)bb;
+  float t0 = 1.5f - f, t1 = f - 1.0f, t2 = f - 0.5f;
+  w[0] = 0.5f * (t0 * t0);
+  w[1] = 0.75f - t1 * t1;
+  w[2] = 0.5f * (t2 * t2);
+  b = bb;
+}
+
+// Exactly-rounded variant (no FMA contraction) used by the deterministic
+// mode; must equal oracle/mpm_oracle.c:stencil_axis32 bit for bit.
+__device__ __forceinline__ void stencil_rn(float xc, float inv_dx, int r, int& b, float& f,
+                                           float w[3]) {
+  float g = __fmul_rn(xc, inv_dx);
+  int bb = (int)floorf(__fsub_rn(g, 0.5f));
+  bb = max(0, min(bb, r - 3));
+  f = __fsub_rn(g, (float)bb);
+  float t0 = __fsub_rn(1.5f, f), t1 = __fsub_rn(f, 1.0f), t2 = __fsub_rn(f, 0.5f);
+  w[0] = __fmul_rn(0.5f, __fmul_rn(t0, t0));
+  w[1] = __fsub_rn(0.75f, __fmul_rn(t1, t1));
+  w[2] = __fmul_rn(0.5f, __fmul_rn(t2, t2));
+  b = bb;
+}
+
+__device__ __forceinline__ float ldf(const Params& p, int field, long long i) {
+  return p.P[(long long)field * p.cap + i];
+}
+__device__ __forceinline__ void stf(const Params& p, int field, long long i, float v) {
+  p.P[(long long)field * p.cap + i] = v;
+}
+
+// F' = (I + dt C) F (kernels.py:213-231), then the Neo-Hookean affine
+// momentum A = m C + k P F'^T (kernels.py:233-275).  Returns det(F').
+template <bool RN>
+__device__ __forceinline__ float affine_update(float F[9], const float C[9], float m, float vol,
+                                               float mu, float lam, float dt, float stress_coef,
+                                               int stress_form, float A[9]);
+
+template <>
+__device__ __forceinline__ float affine_update<false>(float F[9], const float C[9], float m,
+                                                      float vol, float mu, float lam, float dt,
+                                                      float stress_coef, int stress_form,
+                                                      float A[9]) {
+  float f[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      f[3 * r + c] = F[3 * r + c] + dt * (C[3 * r] * F[c] + C[3 * r + 1] * F[3 + c] +
+                                          C[3 * r + 2] * F[6 + c]);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) F[q] = f[q];
+  float cof[9];
+  cof[0] = f[4] * f[8] - f[5] * f[7];
+  cof[1] = f[5] * f[6] - f[3] * f[8];
+  cof[2] = f[3] * f[7] - f[4] * f[6];
+  cof[3] = f[2] * f[7] - f[1] * f[8];
+  cof[4] = f[0] * f[8] - f[2] * f[6];
+  cof[5] = f[1] * f[6] - f[0] * f[7];
+  cof[6] = f[1] * f[5] - f[2] * f[4];
+  cof[7] = f[2] * f[3] - f[0] * f[5];
+  cof[8] = f[0] * f[4] - f[1] * f[3];
+  float det = f[0] * cof[0] + f[1] * cof[1] + f[2] * cof[2];
+  float js = det > 1.0e-6f ? det : 1.0e-6f;
+  float g = (lam * logf(js) - mu) * (det != 0.0f ? 1.0f / det : 0.0f);
+  float k = stress_coef * vol;
+  float P[9];
+  if (stress_form == 0) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) P[3 * r + c] = mu * f[3 * r + c] + g * cof[3 * c + r];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) P[q] = mu * f[q] + g * cof[q];
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      A[3 * r + c] = m * C[3 * r + c] +
+                     k * (P[3 * r] * f[3 * c] + P[3 * r + 1] * f[3 * c + 1] + P[3 * r + 2] * f[3 * c + 2]);
+  return det;
+}
+
+// Round-to-nearest twin of the above (no contraction) for the deterministic
+// mode; mirrors oracle/mpm_oracle.c:orc32_p2g_sorted operation by operation.
+template <>
+__device__ __forceinline__ float affine_update<true>(float F[9], const float C[9], float m,
+                                                     float vol, float mu, float lam, float dt,
+                                                     float stress_coef, int stress_form,
+                                                     float A[9]) {
+  float f[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float s = __fadd_rn(__fadd_rn(__fmul_rn(C[3 * r], F[c]), __fmul_rn(C[3 * r + 1], F[3 + c])),
+                          __fmul_rn(C[3 * r + 2], F[6 + c]));
+      f[3 * r + c] = __fadd_rn(F[3 * r + c], __fmul_rn(dt, s));
+    }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) F[q] = f[q];
+  auto dif = [](float a, float b, float c, float d) { return __fsub_rn(__fmul_rn(a, b), __fmul_rn(c, d)); };
+  float cof[9];
+  cof[0] = dif(f[4], f[8], f[5], f[7]);
+  cof[1] = dif(f[5], f[6], f[3], f[8]);
+  cof[2] = dif(f[3], f[7], f[4], f[6]);
+  float det = __fadd_rn(__fadd_rn(__fmul_rn(f[0], cof[0]), __fmul_rn(f[1], cof[1])), __fmul_rn(f[2], cof[2]));
+  cof[3] = dif(f[2], f[7], f[1], f[8]);
+  cof[4] = dif(f[0], f[8], f[2], f[6]);
+  cof[5] = dif(f[1], f[6], f[0], f[7]);
+  cof[6] = dif(f[1], f[5], f[2], f[4]);
+  cof[7] = dif(f[2], f[3], f[0], f[5]);
+  cof[8] = dif(f[0], f[4], f[1], f[3]);
+  float js = det > 1.0e-6f ? det : 1.0e-6f;
+  float lj = logf(js);
+  float id = det != 0.0f ? __fdiv_rn(1.0f, det) : 0.0f;
+  float g = __fmul_rn(__fsub_rn(__fmul_rn(lam, lj), mu), id);
+  float P[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float cv = stress_form == 0 ? cof[3 * c + r] : cof[3 * r + c];
+      P[3 * r + c] = __fadd_rn(__fmul_rn(mu, f[3 * r + c]), __fmul_rn(g, cv));
+    }
+  float k = __fmul_rn(stress_coef, vol);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float s = __fadd_rn(__fadd_rn(__fmul_rn(P[3 * r], f[3 * c]), __fmul_rn(P[3 * r + 1], f[3 * c + 1])),
+                          __fmul_rn(P[3 * r + 2], f[3 * c + 2]));
+      A[3 * r + c] = __fadd_rn(__fmul_rn(m, C[3 * r + c]), __fmul_rn(k, s));
+    }
+  return det;
+}
+
+}  // namespace mpm

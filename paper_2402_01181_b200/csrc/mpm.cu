@@ -1,0 +1,920 @@
+// mpm.cu -- C ABI (include/softmpm_b200.h) over the sm_100a kernels.
+//
+// One mpm_ctx = one SimState on one device: it owns every device buffer and a
+// private stream; host pointers are borrowed per call.  The fast path keeps
+// particles binned (8^3-cell bins, counting sort) and runs each stretch of
+// substeps as  rebin -> P2G -> [grid op -> fused G2P/P2G] x (L-1) -> grid op
+// -> G2P, with only active bricks visited on the grid.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/softmpm_b200.h"
+#include "kernels.cuh"
+
+using namespace mpm;
+
+struct mpm_ctx {
+  mpm_config cfg{};
+  int dev = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  long long launches = 0;
+
+  // grid
+  long long nbricks = 0;
+  float4* gm = nullptr;
+  float4* gv = nullptr;
+  int* brick_flag = nullptr;
+  int* active_list = nullptr;
+  int* counters = nullptr;  // [0] active_count, [1] nwork
+  int grid_phase = 0;       // 0 momentum view, 1 velocity view, 2 uploaded velocities
+  int grid_dirty = 2;       // 0 clean, 1 active-list bricks dirty, 2 fully dirty
+
+  // particles (double-buffered SoA)
+  long long n = 0, cap = 0;
+  float* P[2] = {nullptr, nullptr};
+  int* mat[2] = {nullptr, nullptr};
+  int* orig[2] = {nullptr, nullptr};
+  int cur = 0;
+  int* key = nullptr;
+  int* rank = nullptr;
+
+  // bins
+  int nbin[3] = {0, 0, 0};
+  int nbins = 0;
+  int* bin_count = nullptr;
+  int* bin_start = nullptr;
+  int4* work = nullptr;
+  long long work_cap = 0;
+  std::vector<int*> scan_tmp;  // per level block sums (two per level)
+  std::vector<long long> scan_len;
+
+  // materials
+  float* mu = nullptr;
+  float* lam = nullptr;
+  int nmat = 0;
+  unsigned long long* inverted = nullptr;
+
+  // colliders
+  int ncol = 0;
+  ColliderGeo* geo = nullptr;
+  ColliderPose* pose = nullptr;
+  int pose_rows = 0, pose_cap = 0;
+  double* sdf = nullptr;
+  std::vector<ColliderGeo> geo_h;
+
+  // deterministic mode
+  long long ncells = 0;
+  int* cell_count = nullptr;
+  int* cell_start = nullptr;
+  int* perm = nullptr;
+  float* payload = nullptr;
+
+  // staging for fp64 transfers
+  double* stage = nullptr;
+  size_t stage_bytes = 0;
+  int* flag = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int fused_blocks = 0;
+
+  // optional per-kernel timing: event pairs per launch, resolved lazily
+  bool timing = false;
+  struct Mark { int kind; cudaEvent_t a, b; };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+namespace {
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);          \
+      return MPM_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+#define LAUNCHED()                                                            \
+  do {                                                                        \
+    ++ctx->launches;                                                          \
+    cudaError_t e_ = cudaGetLastError();                                      \
+    if (e_ != cudaSuccess) {                                                  \
+      ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e_);     \
+      return MPM_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+int fail(mpm_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename T>
+int dalloc(mpm_ctx* ctx, T** ptr, size_t count) {
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)ptr, count * sizeof(T));
+  if (e != cudaSuccess) {
+    ctx->err = std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + "): " + cudaGetErrorString(e);
+    cudaGetLastError();
+    return MPM_ENOMEM;
+  }
+  return 0;
+}
+
+#define TRY(x)              \
+  do {                      \
+    int r_ = (x);           \
+    if (r_) return r_;      \
+  } while (0)
+
+cudaEvent_t pool_event(mpm_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// kind: 0 fused, 1 grid op, 2 rebin, 3 g2p
+struct TimedRegion {
+  mpm_ctx* ctx;
+  int kind;
+  cudaEvent_t a = nullptr;
+  TimedRegion(mpm_ctx* c, int k) : ctx(c), kind(k) {
+    if (ctx->timing) {
+      a = pool_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~TimedRegion() {
+    if (a) {
+      cudaEvent_t b = pool_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->marks.push_back({kind, a, b});
+    }
+  }
+};
+
+void resolve_marks(mpm_ctx* ctx) {
+  if (ctx->marks.empty()) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& mk : ctx->marks) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, mk.a, mk.b);
+    ctx->acc[2 * mk.kind] += ms;
+    ctx->acc[2 * mk.kind + 1] += 1.0;
+    ctx->event_pool.push_back(mk.a);
+    ctx->event_pool.push_back(mk.b);
+  }
+  ctx->marks.clear();
+}
+
+inline unsigned blocks_for(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
+
+Params make_params(mpm_ctx* ctx) {
+  Params p{};
+  const mpm_config& c = ctx->cfg;
+  for (int a = 0; a < 3; ++a) {
+    p.res[a] = c.res[a];
+    p.nb[a] = (c.res[a] + 3) / 4;
+    p.nbin[a] = ctx->nbin[a];
+    p.gravity[a] = (float)c.gravity[a];
+    double hd = (c.res[a] - 1.5 - 1.0e-7) * c.dx;
+    float hf = (float)hd;
+    if ((double)hf > hd) hf = std::nextafter(hf, 0.0f);
+    p.hi[a] = hf;
+  }
+  p.dx = (float)c.dx;
+  p.inv_dx = 1.0f / p.dx;
+  p.dt = (float)c.dt;
+  p.lo = (float)(1.5 * c.dx);
+  p.stress_coef = -4.0f * p.dt * p.inv_dx * p.inv_dx;
+  p.apic_coef = 4.0f * p.inv_dx * p.inv_dx;
+  p.dx64 = c.dx;
+  p.dt64 = c.dt;
+  p.bwidth = c.boundary_width;
+  p.stick = c.stick;
+  p.stress_form = c.stress_form;
+  p.gm = ctx->gm;
+  p.gv = ctx->gv;
+  p.brick_flag = ctx->brick_flag;
+  p.active_list = ctx->active_list;
+  p.active_count = ctx->counters;
+  p.P = ctx->P[ctx->cur];
+  p.mat = ctx->mat[ctx->cur];
+  p.orig = ctx->orig[ctx->cur];
+  p.cap = ctx->cap;
+  p.n = ctx->n;
+  p.mu = ctx->mu;
+  p.lam = ctx->lam;
+  p.inverted = ctx->inverted;
+  p.work = ctx->work;
+  p.nwork = ctx->counters + 1;
+  return p;
+}
+
+Colliders make_colliders(mpm_ctx* ctx, int row, bool use) {
+  Colliders cs{};
+  cs.count = use ? ctx->ncol : 0;
+  cs.theta = use && ctx->ncol > 0 ? ctx->cfg.theta : -1.0;
+  cs.geo = ctx->geo;
+  int r = ctx->pose_rows > 0 ? std::min(row, ctx->pose_rows - 1) : 0;
+  cs.pose = ctx->pose ? ctx->pose + (size_t)r * std::max(ctx->ncol, 1) : nullptr;
+  cs.sdf = ctx->sdf;
+  return cs;
+}
+
+int validate(const mpm_config* c, std::string& why) {
+  for (int a = 0; a < 3; ++a)
+    if (c->res[a] < 8) {
+      why = "grid resolution too small";
+      return 1;
+    }
+  if (!(c->dx > 0.0)) { why = "dx must be positive"; return 1; }
+  if (!(c->dt > 0.0)) { why = "dt must be positive"; return 1; }
+  if (c->boundary_width < 0) { why = "boundary_width must be >= 0"; return 1; }
+  if (c->stress_form != 0 && c->stress_form != 1) { why = "unknown stress form"; return 1; }
+  double nodes = (double)((c->res[0] + 3) / 4) * ((c->res[1] + 3) / 4) * ((c->res[2] + 3) / 4) * 64.0;
+  if (nodes >= 2147483647.0) { why = "grid too large for 32-bit node indexing on one device"; return 1; }
+  return 0;
+}
+
+int alloc_grid(mpm_ctx* ctx) {
+  const mpm_config& c = ctx->cfg;
+  long long nb = (long long)((c.res[0] + 3) / 4) * ((c.res[1] + 3) / 4) * ((c.res[2] + 3) / 4);
+  ctx->nbricks = nb;
+  TRY(dalloc(ctx, &ctx->gm, (size_t)nb * 64));
+  TRY(dalloc(ctx, &ctx->gv, (size_t)nb * 64));
+  TRY(dalloc(ctx, &ctx->brick_flag, (size_t)nb));
+  TRY(dalloc(ctx, &ctx->active_list, (size_t)nb));
+  CK(cudaMemsetAsync(ctx->gm, 0, sizeof(float4) * nb * 64, ctx->stream));
+  CK(cudaMemsetAsync(ctx->gv, 0, sizeof(float4) * nb * 64, ctx->stream));
+  CK(cudaMemsetAsync(ctx->brick_flag, 0, sizeof(int) * nb, ctx->stream));
+  for (int a = 0; a < 3; ++a) ctx->nbin[a] = (c.res[a] + BIN - 1) / BIN;
+  ctx->nbins = ctx->nbin[0] * ctx->nbin[1] * ctx->nbin[2];
+  TRY(dalloc(ctx, &ctx->bin_count, (size_t)ctx->nbins));
+  TRY(dalloc(ctx, &ctx->bin_start, (size_t)ctx->nbins));
+  ctx->grid_dirty = 0;
+  ctx->grid_phase = 0;
+  return 0;
+}
+
+// temp storage for the exclusive scan of up to `n` ints
+int ensure_scan(mpm_ctx* ctx, long long n) {
+  long long need = n;
+  size_t level = 0;
+  while (true) {
+    long long nb = (need + SCAN_TILE - 1) / SCAN_TILE;
+    if (level >= ctx->scan_len.size() || ctx->scan_len[level] < nb) {
+      if (level < ctx->scan_len.size()) {
+        cudaFree(ctx->scan_tmp[2 * level]);
+        cudaFree(ctx->scan_tmp[2 * level + 1]);
+      } else {
+        ctx->scan_len.push_back(0);
+        ctx->scan_tmp.push_back(nullptr);
+        ctx->scan_tmp.push_back(nullptr);
+      }
+      int* a = nullptr;
+      int* b = nullptr;
+      TRY(dalloc(ctx, &a, (size_t)nb));
+      TRY(dalloc(ctx, &b, (size_t)nb));
+      ctx->scan_tmp[2 * level] = a;
+      ctx->scan_tmp[2 * level + 1] = b;
+      ctx->scan_len[level] = nb;
+    }
+    if (nb <= 1) break;
+    need = nb;
+    ++level;
+  }
+  return 0;
+}
+
+int scan_exclusive(mpm_ctx* ctx, const int* in, int* out, long long n, size_t level = 0) {
+  long long nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  int* sums = ctx->scan_tmp[2 * level];
+  int* sums_scanned = ctx->scan_tmp[2 * level + 1];
+  scan_tile_kernel<<<(unsigned)nb, SCAN_THREADS, 0, ctx->stream>>>(in, out, sums, n);
+  LAUNCHED();
+  if (nb > 1) {
+    TRY(scan_exclusive(ctx, sums, sums_scanned, nb, level + 1));
+    scan_add_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(out, sums_scanned, n);
+    LAUNCHED();
+  }
+  return 0;
+}
+
+int ensure_stage(mpm_ctx* ctx, size_t bytes) {
+  if (ctx->stage_bytes >= bytes) return 0;
+  TRY(dalloc(ctx, &ctx->stage, bytes / sizeof(double) + 1));
+  ctx->stage_bytes = bytes;
+  return 0;
+}
+
+int ensure_gm_clean(mpm_ctx* ctx) {
+  if (ctx->grid_dirty == 2) {
+    CK(cudaMemsetAsync(ctx->gm, 0, sizeof(float4) * ctx->nbricks * 64, ctx->stream));
+    CK(cudaMemsetAsync(ctx->brick_flag, 0, sizeof(int) * ctx->nbricks, ctx->stream));
+  } else if (ctx->grid_dirty == 1) {
+    Params p = make_params(ctx);
+    clear_active_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(p);
+    LAUNCHED();
+  }
+  ctx->grid_dirty = 0;
+  return 0;
+}
+
+// Counting sort of particles by 8^3-cell bin + work list (bin, start, end).
+int rebin(mpm_ctx* ctx) {
+  TimedRegion tr(ctx, 2);
+  Params p = make_params(ctx);
+  CK(cudaMemsetAsync(ctx->bin_count, 0, sizeof(int) * ctx->nbins, ctx->stream));
+  CK(cudaMemsetAsync(ctx->counters + 1, 0, sizeof(int), ctx->stream));
+  bin_key_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p, ctx->key, ctx->rank, ctx->bin_count);
+  LAUNCHED();
+  TRY(scan_exclusive(ctx, ctx->bin_count, ctx->bin_start, ctx->nbins));
+  int nxt = ctx->cur ^ 1;
+  permute_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
+      ctx->P[ctx->cur], ctx->mat[ctx->cur], ctx->orig[ctx->cur], ctx->P[nxt], ctx->mat[nxt], ctx->orig[nxt],
+      ctx->key, ctx->rank, ctx->bin_start, ctx->n, ctx->cap);
+  LAUNCHED();
+  ctx->cur = nxt;
+  make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(ctx->bin_count, ctx->bin_start,
+                                                                           ctx->nbins, ctx->work, ctx->counters + 1);
+  LAUNCHED();
+  return 0;
+}
+
+int launch_fused(mpm_ctx* ctx, bool g2p) {
+  Params p = make_params(ctx);
+  size_t smem = sizeof(float4) * TILE_NODES;
+  CK(cudaMemsetAsync(ctx->counters, 0, sizeof(int), ctx->stream));
+  TimedRegion tr(ctx, 0);
+  if (g2p)
+    fused_kernel<true, true><<<ctx->fused_blocks, 256, smem, ctx->stream>>>(p);
+  else
+    fused_kernel<false, true><<<ctx->fused_blocks, 256, smem, ctx->stream>>>(p);
+  LAUNCHED();
+  return 0;
+}
+
+int launch_grid_op(mpm_ctx* ctx, bool dense, bool use_col, int row, bool clear) {
+  Params p = make_params(ctx);
+  Colliders cs = make_colliders(ctx, row, use_col);
+  TimedRegion tr(ctx, 1);
+  if (dense)
+    grid_op_kernel<true><<<ctx->sms * 8, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
+  else
+    grid_op_kernel<false><<<ctx->sms * 8, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
+  LAUNCHED();
+  return 0;
+}
+
+int launch_g2p(mpm_ctx* ctx) {
+  TimedRegion tr(ctx, 3);
+  Params p = make_params(ctx);
+  g2p_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p);
+  LAUNCHED();
+  return 0;
+}
+
+// Deterministic P2G: cell-sorted permutation (ascending cell key, then
+// original index), payload, node-owner gather over every node.
+int det_p2g(mpm_ctx* ctx) {
+  long long ncells = (long long)ctx->cfg.res[0] * ctx->cfg.res[1] * ctx->cfg.res[2];
+  if (ctx->ncells != ncells) {
+    TRY(dalloc(ctx, &ctx->cell_count, (size_t)ncells));
+    TRY(dalloc(ctx, &ctx->cell_start, (size_t)ncells));
+    TRY(ensure_scan(ctx, ncells));
+    ctx->ncells = ncells;
+  }
+  if (!ctx->perm) {
+    TRY(dalloc(ctx, &ctx->perm, (size_t)ctx->cap));
+    TRY(dalloc(ctx, &ctx->payload, (size_t)ctx->cap * 12));
+  }
+  Params p = make_params(ctx);
+  CK(cudaMemsetAsync(ctx->cell_count, 0, sizeof(int) * ncells, ctx->stream));
+  cell_key_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p, ctx->key, ctx->rank, ctx->cell_count);
+  LAUNCHED();
+  TRY(scan_exclusive(ctx, ctx->cell_count, ctx->cell_start, ncells));
+  cell_fill_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(ctx->key, ctx->rank, ctx->cell_start,
+                                                                      ctx->perm, ctx->n);
+  LAUNCHED();
+  cell_sort_kernel<<<blocks_for(ncells, 256), 256, 0, ctx->stream>>>(ctx->cell_count, ctx->cell_start, ctx->perm,
+                                                                      p.orig, ncells);
+  LAUNCHED();
+  det_payload_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p, ctx->payload);
+  LAUNCHED();
+  det_gather_kernel<<<blocks_for(ncells, 256), 256, 0, ctx->stream>>>(p, ctx->payload, ctx->cell_count,
+                                                                       ctx->cell_start, ctx->perm);
+  LAUNCHED();
+  ctx->grid_dirty = 2;
+  return 0;
+}
+
+int need_particles(mpm_ctx* ctx) {
+  if (ctx->n <= 0) return fail(ctx, MPM_ESTATE, "no particles uploaded");
+  if (ctx->nmat <= 0) return fail(ctx, MPM_ESTATE, "no materials set");
+  return 0;
+}
+
+int read_inverted(mpm_ctx* ctx, int64_t* out) {
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, ctx->inverted, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (out) *out = (int64_t)h;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpm_version(void) { return "softmpm_b200 0.1 (sm_100a)"; }
+
+const char* mpm_last_error(mpm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t mpm_launch_count(mpm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
+  if (!out || !cfg) return MPM_EINVAL;
+  *out = nullptr;
+  std::string why;
+  if (validate(cfg, why)) {
+    static thread_local std::string last;
+    last = why;
+    return MPM_EINVAL;
+  }
+  mpm_ctx* ctx = new mpm_ctx();
+  ctx->cfg = *cfg;
+  if (ctx->cfg.rebin_interval < 1) ctx->cfg.rebin_interval = 25;
+  ctx->dev = cfg->device;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    delete ctx;
+    return MPM_ECUDA;
+  }
+  if (cudaSetDevice(ctx->dev) != cudaSuccess) {
+    delete ctx;
+    return MPM_ECUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->dev);
+  int rc = 0;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc) rc = alloc_grid(ctx);
+  if (!rc) rc = dalloc(ctx, &ctx->counters, 4);
+  if (!rc) rc = dalloc(ctx, &ctx->inverted, 1);
+  if (!rc) rc = dalloc(ctx, &ctx->flag, 1);
+  if (!rc) rc = ensure_scan(ctx, ctx->nbins);
+  if (!rc && cudaMemsetAsync(ctx->counters, 0, 16, ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc) {
+    cudaEventCreate(&ctx->ev0);
+    cudaEventCreate(&ctx->ev1);
+    size_t smem = sizeof(float4) * TILE_NODES;
+    cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<true, true>, 256, smem);
+    ctx->fused_blocks = ctx->sms * std::max(1, occ);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
+  }
+  if (rc) {
+    mpm_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return 0;
+}
+
+int mpm_destroy(mpm_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaSetDevice(ctx->dev);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1],
+                  ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
+                  ctx->bin_start, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
+                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (int* b : ctx->scan_tmp)
+    if (b) cudaFree(b);
+  for (auto& mk : ctx->marks) {
+    cudaEventDestroy(mk.a);
+    cudaEventDestroy(mk.b);
+  }
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return 0;
+}
+
+int mpm_set_config(mpm_ctx* ctx, const mpm_config* cfg) {
+  if (!ctx || !cfg) return MPM_EINVAL;
+  std::string why;
+  if (validate(cfg, why)) return fail(ctx, MPM_EINVAL, why);
+  for (int a = 0; a < 3; ++a)
+    if (cfg->res[a] != ctx->cfg.res[a] || cfg->dx != ctx->cfg.dx)
+      return fail(ctx, MPM_EINVAL, "grid geometry cannot change on a live context");
+  int keep_dev = ctx->cfg.device;
+  ctx->cfg = *cfg;
+  ctx->cfg.device = keep_dev;
+  if (ctx->cfg.rebin_interval < 1) ctx->cfg.rebin_interval = 25;
+  return 0;
+}
+
+int mpm_set_materials(mpm_ctx* ctx, const double* mu, const double* lam, int count) {
+  if (!ctx || !mu || !lam || count <= 0) return fail(ctx, MPM_EINVAL, "materials: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  std::vector<float> m(count), l(count);
+  for (int i = 0; i < count; ++i) {
+    m[i] = (float)mu[i];
+    l[i] = (float)lam[i];
+  }
+  if (count != ctx->nmat) {
+    TRY(dalloc(ctx, &ctx->mu, (size_t)count));
+    TRY(dalloc(ctx, &ctx->lam, (size_t)count));
+    ctx->nmat = count;
+  }
+  CK(cudaMemcpyAsync(ctx->mu, m.data(), sizeof(float) * count, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->lam, l.data(), sizeof(float) * count, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double* v, const double* F,
+                         const double* C, const double* mass, const double* vol0, const int32_t* material_id) {
+  if (!ctx || n <= 0 || !x || !v || !F || !C || !mass || !vol0 || !material_id)
+    return fail(ctx, MPM_EINVAL, "upload_particles: bad arguments");
+  if (n >= (1LL << 31) - CHUNK) return fail(ctx, MPM_EINVAL, "too many particles for one context");
+  for (int64_t i = 0; i < n; ++i)
+    if (material_id[i] < 0 || (ctx->nmat > 0 && material_id[i] >= ctx->nmat))
+      return fail(ctx, MPM_EINVAL, "material id out of range");
+  CK(cudaSetDevice(ctx->dev));
+  if (n > ctx->cap) {
+    long long cap = n;
+    for (int b = 0; b < 2; ++b) {
+      TRY(dalloc(ctx, &ctx->P[b], (size_t)cap * NF));
+      TRY(dalloc(ctx, &ctx->mat[b], (size_t)cap));
+      TRY(dalloc(ctx, &ctx->orig[b], (size_t)cap));
+    }
+    TRY(dalloc(ctx, &ctx->key, (size_t)cap));
+    TRY(dalloc(ctx, &ctx->rank, (size_t)cap));
+    ctx->work_cap = ctx->nbins + cap / CHUNK + 1;
+    TRY(dalloc(ctx, &ctx->work, (size_t)ctx->work_cap));
+    if (ctx->perm) {
+      cudaFree(ctx->perm);
+      cudaFree(ctx->payload);
+      ctx->perm = nullptr;
+      ctx->payload = nullptr;
+    }
+    ctx->cap = cap;
+  }
+  ctx->n = n;
+  ctx->cur = 0;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
+  double* s = ctx->stage;
+  CK(cudaMemcpyAsync(s, mass, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(s + n, vol0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(s + 2 * n, material_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  Params p = make_params(ctx);
+  upload_static_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, s, s + n, (const int*)(s + 2 * n));
+  LAUNCHED();
+  return mpm_upload_fields(ctx, MPM_FIELD_ALL, x, v, F, C);
+}
+
+int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double* v, const double* F,
+                      const double* C) {
+  if (!ctx || ctx->n <= 0) return fail(ctx, MPM_ESTATE, "upload_fields: no particles");
+  if (!mask) return 0;
+  CK(cudaSetDevice(ctx->dev));
+  long long n = ctx->n;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
+  double* sx = ctx->stage;
+  double* sv = sx + 3 * n;
+  double* sF = sx + 6 * n;
+  double* sC = sx + 15 * n;
+  if ((mask & MPM_FIELD_X) && x) CK(cudaMemcpyAsync(sx, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  if ((mask & MPM_FIELD_V) && v) CK(cudaMemcpyAsync(sv, v, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  if ((mask & MPM_FIELD_F) && F) CK(cudaMemcpyAsync(sF, F, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, ctx->stream));
+  if ((mask & MPM_FIELD_C) && C) CK(cudaMemcpyAsync(sC, C, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, ctx->stream));
+  unsigned m = (x ? mask & 1u : 0u) | (v ? mask & 2u : 0u) | (F ? mask & 4u : 0u) | (C ? mask & 8u : 0u);
+  Params p = make_params(ctx);
+  upload_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, sx, sv, sF, sC, m);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, double* F, double* C) {
+  if (!ctx || ctx->n <= 0) return fail(ctx, MPM_ESTATE, "download: no particles");
+  CK(cudaSetDevice(ctx->dev));
+  long long n = ctx->n;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
+  double* sx = ctx->stage;
+  double* sv = sx + 3 * n;
+  double* sF = sx + 6 * n;
+  double* sC = sx + 15 * n;
+  unsigned m = (x ? mask & 1u : 0u) | (v ? mask & 2u : 0u) | (F ? mask & 4u : 0u) | (C ? mask & 8u : 0u);
+  Params p = make_params(ctx);
+  download_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, sx, sv, sF, sC, m);
+  LAUNCHED();
+  if (m & 1u) CK(cudaMemcpyAsync(x, sx, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (m & 2u) CK(cudaMemcpyAsync(v, sv, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (m & 4u) CK(cudaMemcpyAsync(F, sF, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (m & 8u) CK(cudaMemcpyAsync(C, sC, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int64_t mpm_particle_count(mpm_ctx* ctx) { return ctx ? ctx->n : 0; }
+
+int mpm_upload_grid(mpm_ctx* ctx, int target, const double* grid_mv, const double* grid_m) {
+  if (!ctx || !grid_mv || (target != 0 && target != 1)) return fail(ctx, MPM_EINVAL, "upload_grid: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  long long nn = (long long)ctx->cfg.res[0] * ctx->cfg.res[1] * ctx->cfg.res[2];
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)nn * 4));
+  CK(cudaMemcpyAsync(ctx->stage, grid_mv, sizeof(double) * 3 * nn, cudaMemcpyHostToDevice, ctx->stream));
+  const double* dm_ = nullptr;
+  if (target == 0) {
+    if (!grid_m) return fail(ctx, MPM_EINVAL, "upload_grid: momentum target needs grid_m");
+    CK(cudaMemcpyAsync(ctx->stage + 3 * nn, grid_m, sizeof(double) * nn, cudaMemcpyHostToDevice, ctx->stream));
+    dm_ = ctx->stage + 3 * nn;
+  }
+  Params p = make_params(ctx);
+  if (target == 0) {
+    upload_grid_kernel<<<blocks_for(nn, 256), 256, 0, ctx->stream>>>(p, ctx->gm, ctx->stage, dm_);
+    LAUNCHED();
+    ctx->grid_phase = 0;
+  } else {
+    // velocities for g2p: keep masses, overwrite gv
+    upload_grid_kernel<<<blocks_for(nn, 256), 256, 0, ctx->stream>>>(p, ctx->gv, ctx->stage, nullptr);
+    LAUNCHED();
+    ctx->grid_phase = 2;
+  }
+  ctx->grid_dirty = 2;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_download_grid(mpm_ctx* ctx, double* grid_mv, double* grid_m) {
+  if (!ctx || !grid_mv) return fail(ctx, MPM_EINVAL, "download_grid: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  long long nn = (long long)ctx->cfg.res[0] * ctx->cfg.res[1] * ctx->cfg.res[2];
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)nn * 4));
+  Params p = make_params(ctx);
+  download_grid_kernel<<<blocks_for(nn, 256), 256, 0, ctx->stream>>>(p, ctx->grid_phase, ctx->stage,
+                                                                      grid_m ? ctx->stage + 3 * nn : nullptr);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(grid_mv, ctx->stage, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, ctx->stream));
+  if (grid_m) CK(cudaMemcpyAsync(grid_m, ctx->stage + 3 * nn, sizeof(double) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_set_colliders(mpm_ctx* ctx, int count, const int32_t* kind, const double* half, const double* rotation,
+                      const double* translation, const double* linear_velocity, const double* angular_velocity,
+                      const double* friction, const int32_t* mode, const double* sdf_values, int64_t sdf_len,
+                      const int64_t* sdf_offset, const int32_t* sdf_resolution, const double* sdf_bounds_min,
+                      const double* sdf_extent) {
+  if (!ctx || count < 0 || count > MAX_COLLIDERS) return fail(ctx, MPM_EINVAL, "set_colliders: bad count");
+  CK(cudaSetDevice(ctx->dev));
+  ctx->ncol = count;
+  ctx->geo_h.assign(std::max(count, 1), ColliderGeo{});
+  std::vector<ColliderPose> pose(std::max(count, 1));
+  for (int i = 0; i < count; ++i) {
+    ColliderGeo& g = ctx->geo_h[i];
+    g.kind = kind[i];
+    if (g.kind != 0 && g.kind != 1) return fail(ctx, MPM_EINVAL, "unknown collider kind");
+    for (int a = 0; a < 3; ++a) {
+      g.half[a] = half[3 * i + a];
+      g.sdf_res[a] = sdf_resolution ? sdf_resolution[3 * i + a] : 0;
+      g.sdf_bmin[a] = sdf_bounds_min ? sdf_bounds_min[3 * i + a] : 0.0;
+    }
+    g.fric = friction[i];
+    g.mode = mode[i];
+    g.sdf_off = sdf_offset ? sdf_offset[i] : -1;
+    g.sdf_ext = sdf_extent ? sdf_extent[i] : 1.0;
+    if (g.kind == 1) {
+      if (!sdf_values || g.sdf_off < 0 || g.sdf_res[0] < 2 || g.sdf_res[1] < 2 || g.sdf_res[2] < 2 ||
+          g.sdf_off + (long long)g.sdf_res[0] * g.sdf_res[1] * g.sdf_res[2] > sdf_len)
+        return fail(ctx, MPM_EINVAL, "baked collider: SDF lattice out of range");
+    }
+    ColliderPose& q = pose[i];
+    for (int a = 0; a < 9; ++a) q.R[a] = rotation[9 * i + a];
+    for (int a = 0; a < 3; ++a) {
+      q.T[a] = translation[3 * i + a];
+      q.lv[a] = linear_velocity[3 * i + a];
+      q.av[a] = angular_velocity[3 * i + a];
+    }
+    q.mode = mode[i];
+  }
+  TRY(dalloc(ctx, &ctx->geo, (size_t)std::max(count, 1)));
+  CK(cudaMemcpyAsync(ctx->geo, ctx->geo_h.data(), sizeof(ColliderGeo) * std::max(count, 1), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (ctx->pose_cap < 1) {
+    TRY(dalloc(ctx, &ctx->pose, (size_t)MAX_COLLIDERS));
+    ctx->pose_cap = 1;
+  }
+  CK(cudaMemcpyAsync(ctx->pose, pose.data(), sizeof(ColliderPose) * std::max(count, 1), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  ctx->pose_rows = 1;
+  if (sdf_values && sdf_len > 0) {
+    TRY(dalloc(ctx, &ctx->sdf, (size_t)sdf_len));
+    CK(cudaMemcpyAsync(ctx->sdf, sdf_values, sizeof(double) * sdf_len, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_set_pose_table(mpm_ctx* ctx, int nsub, const double* rotation, const double* translation,
+                       const double* linear_velocity, const double* angular_velocity, const int32_t* mode) {
+  if (!ctx || nsub <= 0 || !rotation || !translation || !linear_velocity || !angular_velocity)
+    return fail(ctx, MPM_EINVAL, "set_pose_table: bad arguments");
+  if (ctx->ncol <= 0) return 0;
+  CK(cudaSetDevice(ctx->dev));
+  int k = ctx->ncol;
+  std::vector<ColliderPose> rows((size_t)nsub * k);
+  for (int s = 0; s < nsub; ++s)
+    for (int i = 0; i < k; ++i) {
+      size_t r = (size_t)s * k + i;
+      ColliderPose& q = rows[r];
+      for (int a = 0; a < 9; ++a) q.R[a] = rotation[9 * r + a];
+      for (int a = 0; a < 3; ++a) {
+        q.T[a] = translation[3 * r + a];
+        q.lv[a] = linear_velocity[3 * r + a];
+        q.av[a] = angular_velocity[3 * r + a];
+      }
+      q.mode = mode ? mode[r] : ctx->geo_h[i].mode;
+    }
+  if (ctx->pose_cap < nsub) {
+    TRY(dalloc(ctx, &ctx->pose, (size_t)nsub * MAX_COLLIDERS));
+    ctx->pose_cap = nsub;
+  }
+  CK(cudaMemcpyAsync(ctx->pose, rows.data(), sizeof(ColliderPose) * rows.size(), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->pose_rows = nsub;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_p2g(mpm_ctx* ctx, int64_t* inverted) {
+  if (!ctx) return MPM_EINVAL;
+  TRY(need_particles(ctx));
+  CK(cudaSetDevice(ctx->dev));
+  CK(cudaMemsetAsync(ctx->inverted, 0, sizeof(unsigned long long), ctx->stream));
+  if (ctx->cfg.deterministic) {
+    TRY(det_p2g(ctx));
+  } else {
+    ctx->grid_dirty = 2;  // stage p2g overwrites the whole grid (p2g_reduce writes every node)
+    TRY(ensure_gm_clean(ctx));
+    TRY(rebin(ctx));
+    TRY(launch_fused(ctx, false));
+    ctx->grid_dirty = 2;
+  }
+  ctx->grid_phase = 0;
+  return read_inverted(ctx, inverted);
+}
+
+int mpm_grid_update(mpm_ctx* ctx, int use_colliders) {
+  if (!ctx) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->grid_phase == 2) return fail(ctx, MPM_ESTATE, "grid holds velocities; run p2g first");
+  TRY(launch_grid_op(ctx, true, use_colliders != 0, 0, false));
+  ctx->grid_phase = 1;
+  ctx->grid_dirty = 2;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_g2p(mpm_ctx* ctx) {
+  if (!ctx) return MPM_EINVAL;
+  TRY(need_particles(ctx));
+  CK(cudaSetDevice(ctx->dev));
+  TRY(launch_g2p(ctx));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, double* device_ms) {
+  if (!ctx || nsub <= 0) return fail(ctx, MPM_EINVAL, "substeps: nsub must be >= 1");
+  TRY(need_particles(ctx));
+  CK(cudaSetDevice(ctx->dev));
+  bool col = use_colliders && ctx->ncol > 0 && ctx->cfg.theta >= 0.0;
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  CK(cudaMemsetAsync(ctx->inverted, 0, sizeof(unsigned long long), ctx->stream));
+  if (ctx->cfg.deterministic) {
+    for (int s = 0; s < nsub; ++s) {
+      TRY(det_p2g(ctx));
+      TRY(launch_grid_op(ctx, true, col, s, false));
+      TRY(launch_g2p(ctx));
+    }
+    ctx->grid_dirty = 2;
+  } else {
+    TRY(ensure_gm_clean(ctx));
+    int s = 0;
+    while (s < nsub) {
+      int L = std::min(ctx->cfg.rebin_interval, nsub - s);
+      TRY(rebin(ctx));
+      for (int t = 0; t < L; ++t) {
+        TRY(launch_fused(ctx, t > 0));
+        TRY(launch_grid_op(ctx, false, col, s + t, s + t != nsub - 1));
+      }
+      TRY(launch_g2p(ctx));
+      s += L;
+    }
+    ctx->grid_dirty = 1;
+  }
+  ctx->grid_phase = 1;
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  TRY(read_inverted(ctx, inverted));
+  if (device_ms) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    *device_ms = ms;
+  }
+  return 0;
+}
+
+int mpm_collision_field(mpm_ctx* ctx, double theta, double* dist, int32_t* obj) {
+  if (!ctx || !dist || !obj) return fail(ctx, MPM_EINVAL, "collision_field: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  long long nn = (long long)ctx->cfg.res[0] * ctx->cfg.res[1] * ctx->cfg.res[2];
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)nn * 2));
+  Params p = make_params(ctx);
+  Colliders cs = make_colliders(ctx, 0, true);
+  cs.theta = theta;
+  collision_field_kernel<<<blocks_for(nn, 256), 256, 0, ctx->stream>>>(p, cs, 2.0 * theta, ctx->stage,
+                                                                        (int*)(ctx->stage + nn));
+  LAUNCHED();
+  CK(cudaMemcpyAsync(dist, ctx->stage, sizeof(double) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(obj, ctx->stage + nn, sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_has_nan(mpm_ctx* ctx, int* flag) {
+  if (!ctx || !flag) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  *flag = 0;
+  if (ctx->n <= 0) return 0;
+  CK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+  Params p = make_params(ctx);
+  has_nan_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p, ctx->flag);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(flag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_set_timing(mpm_ctx* ctx, int enable) {
+  if (!ctx) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  resolve_marks(ctx);
+  ctx->timing = enable != 0;
+  for (double& a : ctx->acc) a = 0.0;
+  return 0;
+}
+
+int mpm_get_timing(mpm_ctx* ctx, double* out) {
+  if (!ctx || !out) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  resolve_marks(ctx);
+  for (int i = 0; i < 8; ++i) out[i] = ctx->acc[i];
+  int h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, ctx->counters, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  out[8] = h[0];
+  out[9] = h[1];
+  for (double& a : ctx->acc) a = 0.0;
+  return 0;
+}
+
+void* mpm_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, (size_t)bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void mpm_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
+}  // extern "C"

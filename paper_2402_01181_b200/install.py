@@ -1,0 +1,128 @@
+"""Route the reference package's hot path through the B200 kernels.
+
+``install(softmpm)`` rebinds ``softmpm.core.p2g / grid_update / g2p_advect /
+substep / step`` (and the ``softmpm`` top-level re-exports) so unmodified
+callers -- ``cli.simulate`` (cli.py:71), ``cli.cmd_bench`` (cli.py:187-191),
+``server.Session.run_frame`` (server.py:407), ``oracle.oracle_divergence``,
+the demos -- run on the GPU while their ``SimState`` stays the reference's
+numpy dataclass.  Every call uploads the reference state's host arrays into a
+device context cached on the state object and downloads the results back into
+those same arrays (the e2e host-buffer path).  ``uninstall()`` restores the
+originals.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import core as _core
+from .collision import pack_colliders as _pack
+
+_SAVED: dict = {}
+
+
+def _shadow(ref_state):
+    """Device-side SimState mirroring a reference SimState (same arrays by value)."""
+    sh = getattr(ref_state, "_b200_shadow", None)
+    g = ref_state.grid
+    if sh is None or sh.particle_count != len(ref_state.x):
+        sh = _core.SimState(_core.Grid(g.resolution, g.extent), ref_state.x, ref_state.v,
+                            ref_state.F, ref_state.C, ref_state.mass, ref_state.vol0,
+                            ref_state.material_id)
+        ref_state._b200_shadow = sh
+    else:
+        for nm in ("x", "v", "F", "C"):
+            setattr(sh, nm, getattr(ref_state, nm))
+        sh.mass, sh.vol0, sh.material_id = ref_state.mass, ref_state.vol0, ref_state.material_id
+    sh.time = ref_state.time
+    sh.step_count = ref_state.step_count
+    return sh
+
+
+def _writeback(ref_state, sh, fields=("x", "v", "F", "C"), grid=True):
+    for nm in fields:
+        np.copyto(getattr(ref_state, nm), getattr(sh, nm))
+    if grid:
+        np.copyto(ref_state.grid_mv, sh.grid_mv)
+        np.copyto(ref_state.grid_m, sh.grid_m)
+    ref_state.time = sh.time
+    ref_state.step_count = sh.step_count
+
+
+def _params(p):
+    return _core.SimParams(dt=p.dt, substeps_per_frame=p.substeps_per_frame, gravity=tuple(p.gravity),
+                           boundary_width=p.boundary_width, boundary=p.boundary,
+                           collision_theta=p.collision_theta,
+                           accumulation_chunks=p.accumulation_chunks)
+
+
+def _mats(materials):
+    from .materials import Material
+    return [Material(m.young_modulus, m.poisson_ratio, m.density) for m in materials]
+
+
+def install(softmpm_module):
+    """Patch the reference package in place; returns the module."""
+    core = softmpm_module.core
+    if _SAVED:
+        return softmpm_module
+    for name in ("p2g", "grid_update", "g2p_advect", "substep", "step"):
+        _SAVED[name] = (getattr(core, name), getattr(softmpm_module, name, None))
+
+    def p2g(state, materials, params):
+        sh = _shadow(state)
+        inv = _core.p2g(sh, _mats(materials), _params(params))
+        _writeback(state, sh, ("F",))
+        return inv
+
+    def grid_update(state, params, collision=None, colliders=None):
+        sh = _shadow(state)
+        sh.grid_mv = state.grid_mv
+        sh.grid_m = state.grid_m
+        _core.grid_update(sh, _params(params), collision, _colliders(state, colliders))
+        _writeback(state, sh, ())
+
+    def g2p_advect(state, params):
+        sh = _shadow(state)
+        sh.grid_mv = state.grid_mv
+        _core.g2p_advect(sh, _params(params))
+        _writeback(state, sh, ("x", "v", "C"), grid=False)
+
+    def substep(state, materials, params, colliders=None):
+        sh = _shadow(state)
+        inv = _core.substep(sh, _mats(materials), _params(params), _colliders(state, colliders))
+        _writeback(state, sh)
+        return inv
+
+    def step(state, materials, params, colliders=None, pose_fn=None):
+        sh = _shadow(state)
+        rep = _core.step(sh, _mats(materials), _params(params), _colliders(state, colliders),
+                         pose_fn)
+        _writeback(state, sh)
+        return softmpm_module.core.StepReport(rep.step_index, rep.sim_time, rep.timings_ms,
+                                              rep.inverted_particles)
+
+    for name, fn in (("p2g", p2g), ("grid_update", grid_update), ("g2p_advect", g2p_advect),
+                     ("substep", substep), ("step", step)):
+        setattr(core, name, fn)
+        if hasattr(softmpm_module, name):
+            setattr(softmpm_module, name, fn)
+    return softmpm_module
+
+
+def _colliders(state, colliders):
+    # reference RigidCollider objects carry the same fields; they are used as-is
+    # (pack_colliders only reads attributes), keeping identity for F7 caching
+    return colliders or []
+
+
+def uninstall(softmpm_module):
+    core = softmpm_module.core
+    for name, (orig_core, orig_top) in _SAVED.items():
+        setattr(core, name, orig_core)
+        if orig_top is not None:
+            setattr(softmpm_module, name, orig_top)
+    _SAVED.clear()
+
+
+__all__ = ["install", "uninstall", "_pack"]

@@ -1,0 +1,77 @@
+"""Synthetic tissue scenes of BASELINE.json's configs.
+
+Defaults follow the reference scenarios (scenarios.py:62-64: E = 1e4 Pa,
+nu = 0.3, rho = 1000) and SimParams (dt 5e-4, 25 substeps, clamp boundary
+width 3, theta = 0.5 dx).  Each builder returns (state, materials, params,
+colliders, pose_fn).
+
+  c1  30 K block dropped into the floor band, 64^3, no tools
+  c2  30 K block, 128^3, two baked-SDF capsule jaws (grasper) on a
+      down -> close -> pull keyframe path, Coulomb mu = 0.35 (sticky when closed)
+  c3  1 M slab on 256^3 pressed by a box tool moving down at 0.5 m/s
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .collision import Baked, Box, RigidCollider
+from .core import Grid, SimParams, SimState
+from .materials import Material
+from .sampling import sample_box
+from .scene import GripperGroup, Keyframe, make_pose_fn
+from .sdf import bake_capsule
+
+_Q = np.array([0.0, 0.0, 0.0, 1.0])
+
+
+def _material():
+    return [Material(1.0e4, 0.3, 1000.0)]
+
+
+def c1(count: int = 30_000, res: int = 64, seed: int = 1):
+    grid = Grid((res, res, res))
+    mats = _material()
+    spawn = sample_box((0.5, 0.13, 0.5), (0.3, 0.2, 0.3), count, seed=seed, grid=grid)
+    st = SimState.from_spawns(grid, [spawn], mats)
+    return st, mats, SimParams(), [], None
+
+
+def c2(count: int = 30_000, res: int = 128, seed: int = 1, sdf_res: int = 64):
+    grid = Grid((res, res, res))
+    mats = _material()
+    spawn = sample_box((0.5, 0.13, 0.5), (0.3, 0.2, 0.3), count, seed=seed, grid=grid)
+    st = SimState.from_spawns(grid, [spawn], mats)
+    jaw = bake_capsule(radius=0.02, half_length=0.06, resolution=sdf_res, axis=1)
+    cols = [RigidCollider(id=0, shape=Baked(jaw), friction_mu=0.35),
+            RigidCollider(id=1, shape=Baked(jaw), friction_mu=0.35)]
+    half_gap_open, half_gap_closed = 0.07, 0.035
+    waypoints = [(0.0, (0.5, 0.40, 0.5), "open"), (0.25, (0.5, 0.26, 0.5), "open"),
+                 (0.35, (0.5, 0.26, 0.5), "closed"), (0.8, (0.5, 0.42, 0.5), "closed")]
+    traj = []
+    for t, c, jawstate in waypoints:
+        g = half_gap_closed if jawstate == "closed" else half_gap_open
+        c = np.asarray(c)
+        traj.append(Keyframe(t, [(c - [g, 0, 0], _Q), (c + [g, 0, 0], _Q)], jawstate))
+    pose_fn = make_pose_fn(traj, [GripperGroup("grasper", [0, 1])], {0: "coulomb", 1: "coulomb"})
+    pose_fn(cols, 0.0)
+    return st, mats, SimParams(), cols, pose_fn
+
+
+def c3(count: int = 1_000_000, res: int = 256, seed: int = 1):
+    grid = Grid((res, res, res))
+    mats = _material()
+    spawn = sample_box((0.5, 0.1, 0.5), (0.5, 0.0977, 0.5), count, seed=seed, grid=grid)
+    st = SimState.from_spawns(grid, [spawn], mats)
+    top = 0.1 + 0.5 * 0.0977
+    half = np.array([0.08, 0.03, 0.08])
+    y0 = top + half[1] + 0.005
+    traj = [Keyframe(0.0, [(np.array([0.5, y0, 0.5]), _Q)]),
+            Keyframe(0.2, [(np.array([0.5, y0 - 0.1, 0.5]), _Q)])]
+    cols = [RigidCollider(id=0, shape=Box(half), friction_mu=0.4)]
+    pose_fn = make_pose_fn(traj)
+    pose_fn(cols, 0.0)
+    return st, mats, SimParams(), cols, pose_fn
+
+
+BUILDERS = {"c1": c1, "c2": c2, "c3": c3}

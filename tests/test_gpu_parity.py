@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle / golden
+vectors produced by the reference.  Tolerances (BASELINE north star): fp32
+relative-L2 of x, v, F <= 1e-5 after one substep and <= 1e-3 after 100;
+C is compared as |dC| dx / |v| (C's fp64 value under rigid motion
+is cancellation residue).  Grid mass is bit-exact against the fp32
+deterministic-order oracle O3 in deterministic mode."""
+import numpy as np
+import pytest
+
+import paper_2402_01181_b200 as sm
+from conftest import load_golden, packed_from_golden, rel_l2
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_1 = 1e-5
+TOL_100 = 1e-3
+
+
+def _state_from_golden(g, prefix="in"):
+    res = tuple(int(r) for r in g["res"])
+    grid = sm.Grid(res, tuple(float(e) for e in g["extent"]))
+    n = len(g[f"{prefix}_x"])
+    st = sm.SimState(grid, g[f"{prefix}_x"], g[f"{prefix}_v"], g[f"{prefix}_F"], g[f"{prefix}_C"],
+                     g["mass"], g["vol0"], np.zeros(n, np.int32))
+    mats = [sm.Material(float(g["E"]), float(g["nu"]), float(g["rho"]))]
+    return st, mats
+
+
+def _c_err(C, C_ref, v_ref, dx):
+    return float(np.linalg.norm(C - C_ref) * dx / max(np.linalg.norm(v_ref), 1e-30))
+
+
+def _colliders_from_packed(p):
+    cols = []
+    for i in range(len(p.kind)):
+        if p.kind[i] == 0:
+            shape = sm.Box(p.half[i])
+        else:
+            r = tuple(int(a) for a in p.sdf_resolution[i])
+            off = int(p.sdf_offset[i])
+            vals = p.sdf_values[off:off + r[0] * r[1] * r[2]].reshape(r, order="F")
+            shape = sm.Baked(sm.SdfGrid(np.ascontiguousarray(vals), p.sdf_bounds_min[i],
+                                        float(p.sdf_extent[i])))
+        cols.append(sm.RigidCollider(id=i, shape=shape, rotation=p.rotation[i],
+                                     translation=p.translation[i],
+                                     linear_velocity=p.linear_velocity[i],
+                                     angular_velocity=p.angular_velocity[i],
+                                     friction_mu=float(p.friction[i]),
+                                     mode="sticky" if p.mode[i] else "coulomb"))
+    return cols
+
+
+def test_stage_ops_match_reference():
+    g = load_golden("stage_ops.npz")
+    st, mats = _state_from_golden(g)
+    params = sm.SimParams()
+    inv = sm.p2g(st, mats, params)
+    assert inv == int(g["p2g_inverted"])
+    assert rel_l2(st.F, g["p2g_F"]) < TOL_1
+    assert np.abs(st.grid_m - g["p2g_grid_m"]).max() <= 1e-6 * g["p2g_grid_m"].max()
+    assert rel_l2(st.grid_mv, g["p2g_grid_mv"]) < 1e-5
+    sm.grid_update(st, params)
+    assert rel_l2(st.grid_mv, g["gu_grid_mv"]) < 1e-5
+    sm.g2p_advect(st, params)
+    assert rel_l2(st.x, g["g2p_x"]) < TOL_1
+    assert rel_l2(st.v, g["g2p_v"]) < TOL_1
+    assert _c_err(st.C, g["g2p_C"], g["g2p_v"], st.grid.dx) < TOL_1
+
+
+def test_substep_with_box_and_baked_colliders_matches_reference():
+    g = load_golden("substep_colliders.npz")
+    st, mats = _state_from_golden(g)
+    cols = _colliders_from_packed(packed_from_golden(g))
+    params = sm.SimParams()
+    inv = sm.substep(st, mats, params, cols)
+    assert inv == int(g["s1_inverted"])
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), g[f"s1_{k}"]) < TOL_1, k
+    assert _c_err(st.C, g["s1_C"], g["s1_v"], st.grid.dx) < TOL_1
+    assert np.abs(st.grid_m - g["s1_grid_m"]).max() <= 1e-6 * g["s1_grid_m"].max()
+    assert rel_l2(st.grid_mv, g["s1_grid_mv"]) < 1e-4
+    fld = st._collision
+    assert np.array_equal(fld.object_id, g["s1_obj"])
+    assert np.array_equal(fld.distance, g["s1_dist"])
+    for _ in range(9):
+        sm.substep(st, mats, params, cols)
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), g[f"s10_{k}"]) < 1e-4, k
+
+
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_floor_block_trajectory_within_tolerance(deterministic):
+    g = load_golden("floor_block.npz")
+    st, mats = _state_from_golden(g)
+    params = sm.SimParams(deterministic=deterministic, rebin_interval=7)
+    for it in range(1, 101):
+        sm.substep(st, mats, params) if it <= 10 else None
+        if it == 1:
+            for k in ("x", "v", "F"):
+                assert rel_l2(getattr(st, k), g[f"s1_{k}"]) < TOL_1, k
+        if it == 10:
+            for k in ("x", "v", "F"):
+                assert rel_l2(getattr(st, k), g[f"s10_{k}"]) < 1e-4, k
+            break
+    # substeps 11..100 through the fused frame driver (4 frames x 25 - 10)
+    params2 = sm.SimParams(deterministic=deterministic, substeps_per_frame=30, rebin_interval=7)
+    for _ in range(3):
+        sm.step(st, mats, params2)
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), g[f"s100_{k}"]) < TOL_100, k
+    assert st.time == pytest.approx(100 * 5e-4, rel=1e-12)
+
+
+def test_spec_stress_form_matches_loop_nest_oracle():
+    g = load_golden("spec_reference.npz")
+    st, mats = _state_from_golden(g)
+    params = sm.SimParams(stress_form="spec")
+    for _ in range(5):
+        sm.substep(st, mats, params)
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), g[f"s5_{k}"]) < 1e-5, k
+
+
+def test_deterministic_mode_grid_mass_bit_exact_against_o3():
+    g = load_golden("floor_block.npz")
+    st, mats = _state_from_golden(g)
+    # perturb so many particles share cells with nontrivial stencils
+    params = sm.SimParams(deterministic=True)
+    sm.p2g(st, mats, params)
+    x32 = np.float32(g["in_x"])
+    res = tuple(int(r) for r in g["res"])
+    dx = float(g["extent"][0]) / res[0]
+    order = O.sorted_order(x32, dx, res)
+    m = mats[0]
+    gmv, gm, F32, inv = O.p2g_sorted_fp32(g["in_x"], g["in_v"], g["in_F"], g["in_C"], g["mass"],
+                                          g["vol0"], np.zeros(len(order), np.int32), m.mu, m.lam,
+                                          5e-4, dx, res, order)
+    assert np.array_equal(st.grid_m.astype(np.float32), gm)
+    assert np.array_equal(st.grid_m, gm.astype(np.float64))
+    assert rel_l2(st.grid_mv, gmv) < 1e-6
+    # run twice from the same inputs: bitwise identical
+    st2, _ = _state_from_golden(g)
+    sm.p2g(st2, mats, params)
+    assert np.array_equal(st2.grid_m, st.grid_m)
+    assert np.array_equal(st2.grid_mv, st.grid_mv)
+
+
+def test_deterministic_mode_whole_substeps_reproducible():
+    g = load_golden("substep_colliders.npz")
+    outs = []
+    for _ in range(2):
+        st, mats = _state_from_golden(g)
+        cols = _colliders_from_packed(packed_from_golden(g))
+        params = sm.SimParams(deterministic=True)
+        for _ in range(5):
+            sm.substep(st, mats, params, cols)
+        outs.append((st.x.copy(), st.F.copy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_collision_field_matches_oracle_on_random_scenes(rng):
+    from scipy.spatial.transform import Rotation
+    grid = sm.Grid((24, 24, 24))
+    cap = sm.bake_capsule(0.05, 0.1, resolution=24)
+    for _ in range(4):
+        cols = [sm.RigidCollider(id=i, shape=sm.Box(rng.uniform(0.05, 0.3, 3)),
+                                 rotation=Rotation.random(random_state=rng.integers(1 << 30)).as_matrix(),
+                                 translation=rng.uniform(0.1, 0.9, 3)) for i in range(3)]
+        cols.append(sm.RigidCollider(id=3, shape=sm.Baked(cap),
+                                     rotation=Rotation.random(random_state=rng.integers(1 << 30)).as_matrix(),
+                                     translation=rng.uniform(0.3, 0.7, 3)))
+        theta = 0.5 * grid.dx
+        fld = sm.update_collision_field(cols, grid, theta)
+        sim = O.OracleSim(O.OracleParams(res=grid.resolution, dx=grid.dx), np.zeros((1, 3)),
+                          np.zeros((1, 3)), np.zeros((1, 3, 3)), np.zeros((1, 3, 3)), np.ones(1),
+                          np.ones(1), np.zeros(1, np.int32), 1.0, 1.0)
+        dist, obj = sim.collision_field(sm.pack_colliders(cols), theta)
+        assert np.array_equal(fld.object_id, obj)
+        assert np.array_equal(fld.distance, dist)
+
+
+def test_step_with_pose_fn_matches_oracle_per_substep_poses():
+    """Moving box tool driven by a keyframe trajectory: GPU step() vs O1 fed
+    the same per-substep poses (pose_fn replayed at the accumulated times)."""
+    grid = sm.Grid((48, 48, 48))
+    mats = [sm.Material(1e4, 0.3, 1000.0)]
+    spawn = sm.sample_box((0.5, 0.12, 0.5), (0.4, 0.12, 0.4), 6000, seed=4, grid=grid)
+    st = sm.SimState.from_spawns(grid, [spawn], mats)
+    q = np.array([0.0, 0.0, 0.0, 1.0])
+    traj = [sm.Keyframe(0.0, [(np.array([0.5, 0.28, 0.5]), q)]),
+            sm.Keyframe(0.1, [(np.array([0.5, 0.15, 0.5]), q)])]
+    cols = [sm.RigidCollider(id=0, shape=sm.Box(np.array([0.08, 0.04, 0.08])), friction_mu=0.4)]
+    pose_fn = sm.make_pose_fn(traj)
+    pose_fn(cols, 0.0)
+    params = sm.SimParams()
+    op = O.OracleParams(res=grid.resolution, dx=grid.dx, theta=0.5 * grid.dx)
+    osim = O.OracleSim(op, st.x, st.v, st.F, st.C, st.mass, st.vol0, st.material_id, mats[0].mu,
+                       mats[0].lam)
+    ocols = [sm.RigidCollider(id=0, shape=sm.Box(np.array([0.08, 0.04, 0.08])), friction_mu=0.4)]
+    t = 0.0
+    for frame in range(4):
+        rep = sm.step(st, mats, params, cols, pose_fn)
+        for _ in range(params.substeps_per_frame):
+            pose_fn(ocols, t)
+            osim.substep(sm.pack_colliders(ocols))
+            t += params.dt
+    assert rep.step_index == 4
+    assert st.time == t
+    contact = int((st._collision.object_id >= 0).sum())
+    assert contact > 0
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), getattr(osim, k)) < TOL_100, k
+    assert not st.has_nan()
+
+
+def test_large_scene_properties():
+    """C3-sized slab (1M particles, 256^3): conservation and sanity at full size."""
+    grid = sm.Grid((256, 256, 256))
+    mats = [sm.Material(1e4, 0.3, 1000.0)]
+    spawn = sm.sample_box((0.5, 0.1, 0.5), (0.5, 0.0977, 0.5), 1_000_000, seed=1, grid=grid)
+    st = sm.SimState.from_spawns(grid, [spawn], mats)
+    rng = np.random.default_rng(0)
+    st.v = rng.normal(0, 0.05, (len(spawn.positions), 3))
+    params = sm.SimParams(gravity=(0.0, 0.0, 0.0))
+    mom0 = (st.mass[:, None] * st.v).sum(axis=0)
+    sm.p2g(st, mats, params)
+    gm = st.grid_m
+    assert abs(gm.sum() - st.mass.sum()) / st.mass.sum() < 1e-5
+    gmom = st.grid_mv.reshape(-1, 3).sum(axis=0)
+    assert np.linalg.norm(gmom - mom0) / np.linalg.norm(mom0) < 1e-4
+    params = sm.SimParams()
+    for _ in range(2):
+        sm.step(st, mats, params)
+    assert not st.has_nan()
+    lo, hi = grid.margin_bounds()
+    x = st.x
+    assert (x >= lo - 1e-6).all() and (x <= hi + 1e-6).all()
