@@ -25,7 +25,13 @@ constexpr int BIN_SHIFT = 3;
 constexpr int MARGIN = 2;                 // tile margin for particles drifting out of their bin
 constexpr int TILE = BIN + 2 + 2 * MARGIN;  // 14 nodes per tile edge
 constexpr int TILE_NODES = TILE * TILE * TILE;
-constexpr int CHUNK = 2048;               // max particles per work item
+constexpr int FUSED_THREADS = 256;      // stage A (g2p_stress_kernel)
+constexpr int P2G_THREADS = 256;        // stage B (p2g_tile_kernel)
+constexpr int P2G_MIN_BLOCKS = 3;
+constexpr int NPAY = 12;                // payload floats per particle: m v (3), A (9)
+constexpr int CHUNK = 1024;               // max particles per work item (fixed-point headroom, see channel_scale)
+// 4^3 layout bricks overlapped by a tile: org = 8b - MARGIN is even, so a tile edge of TILE nodes spans
+constexpr int TILE_BRICKS = (TILE + 3 + 3) / 4;
 constexpr int NF = 26;                    // float fields per particle
 
 enum Field : int { FX = 0, FV = 3, FF = 6, FC = 15, FMASS = 24, FVOL = 25 };

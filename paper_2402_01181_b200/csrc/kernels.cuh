@@ -42,48 +42,109 @@ __device__ __forceinline__ void axis_offsets(int b, int stride_brick, int stride
   }
 }
 
-// G2P gather at x (kernels.py:451-516): v = sum w g, C = 4/dx^2 sum w g dp^T.
-__device__ __forceinline__ void g2p_gather(const Params& p, const float x[3], float v[3],
+// Velocity sources for the G2P gather: the blocked global grid (through L1)
+// or a shared-memory SoA tile of the work item's node box.
+struct GlobalVel {
+  const float4* gv;
+  int sx, sy;  // brick strides (x: nb1*nb2*64, y: nb2*64)
+  __device__ __forceinline__ void offsets(const int b[3], int ox[3], int oy[3], int oz[3]) const {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      ox[q] = ((b[0] + q) >> BRICK_SHIFT) * sx + ((b[0] + q) & 3) * 16;
+      oy[q] = ((b[1] + q) >> BRICK_SHIFT) * sy + ((b[1] + q) & 3) * 4;
+      oz[q] = ((b[2] + q) >> BRICK_SHIFT) * 64 + ((b[2] + q) & 3);
+    }
+  }
+  __device__ __forceinline__ float3 load(int idx) const {
+    const float4 g = __ldg(gv + idx);
+    return make_float3(g.x, g.y, g.z);
+  }
+};
+
+struct TileVel {
+  const float* t;  // 3 x TILE_NODES floats (vx | vy | vz)
+  int org[3];
+  int lo[3], hi[3];  // loaded base-cell box (tile coords); nodes [lo, hi + 2]
+  __device__ __forceinline__ void offsets(const int b[3], int ox[3], int oy[3], int oz[3]) const {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      ox[q] = (b[0] - org[0] + q) * TILE * TILE;
+      oy[q] = (b[1] - org[1] + q) * TILE;
+      oz[q] = (b[2] - org[2] + q);
+    }
+  }
+  __device__ __forceinline__ float3 load(int idx) const {
+    return make_float3(t[idx], t[TILE_NODES + idx], t[2 * TILE_NODES + idx]);
+  }
+};
+
+// G2P gather (kernels.py:451-516): v = sum w g, C = 4/dx^2 sum w g dp^T,
+// evaluated separably (k, then j, then i sums): 279 FMA instead of 432.
+template <class Src>
+__device__ __forceinline__ void g2p_gather(const Params& p, const Src& src, const int b[3],
+                                           const float f[3], const float w[3][3], float v[3],
                                            float C[9]) {
+  int ox[3], oy[3], oz[3];
+  src.offsets(b, ox, oy, oz);
+  float wd[3][3];  // w * (offset - f)
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) wd[a][q] = w[a][q] * ((float)q - f[a]);
+  float c0[3] = {0.f, 0.f, 0.f}, c1[3] = {0.f, 0.f, 0.f}, c2[3] = {0.f, 0.f, 0.f};
+  v[0] = v[1] = v[2] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float hv[3] = {0.f, 0.f, 0.f}, hj[3] = {0.f, 0.f, 0.f}, hk[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float gv[3] = {0.f, 0.f, 0.f}, gk[3] = {0.f, 0.f, 0.f};
+      const int oij = ox[i] + oy[j];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float3 g = src.load(oij + oz[k]);
+        gv[0] += w[2][k] * g.x; gv[1] += w[2][k] * g.y; gv[2] += w[2][k] * g.z;
+        gk[0] += wd[2][k] * g.x; gk[1] += wd[2][k] * g.y; gk[2] += wd[2][k] * g.z;
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        hv[r] += w[1][j] * gv[r];
+        hj[r] += wd[1][j] * gv[r];
+        hk[r] += w[1][j] * gk[r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      v[r] += w[0][i] * hv[r];
+      c0[r] += wd[0][i] * hv[r];
+      c1[r] += w[0][i] * hj[r];
+      c2[r] += w[0][i] * hk[r];
+    }
+  }
+  const float cc = 4.0f * p.inv_dx;  // coef * dx = 4/dx
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    C[3 * r] = c0[r] * cc;
+    C[3 * r + 1] = c1[r] * cc;
+    C[3 * r + 2] = c2[r] * cc;
+  }
+}
+
+__device__ __forceinline__ GlobalVel global_vel(const Params& p) {
+  GlobalVel s;
+  s.gv = p.gv;
+  s.sx = p.nb[1] * p.nb[2] * 64;
+  s.sy = p.nb[2] * 64;
+  return s;
+}
+
+// G2P at x from the global grid (stage g2p_advect / final G2P of a frame).
+__device__ __forceinline__ void g2p_gather(const Params& p, const float x[3], float v[3], float C[9]) {
   int b[3];
   float f[3], w[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) stencil(x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
-  int ox[3], oy[3], oz[3];
-  axis_offsets(b[0], p.nb[1] * p.nb[2] * 64, 16, ox);
-  axis_offsets(b[1], p.nb[2] * 64, 4, oy);
-  axis_offsets(b[2], 64, 1, oz);
-  float S[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) S[q] = 0.f;
-  v[0] = v[1] = v[2] = 0.f;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    float di = (float)i - f[0];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      float wij = w[0][i] * w[1][j];
-      float dj = (float)j - f[1];
-      int oij = ox[i] + oy[j];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        float wt = wij * w[2][k];
-        float dk = (float)k - f[2];
-        float4 g = __ldg(p.gv + (oij + oz[k]));
-        float wg[3] = {wt * g.x, wt * g.y, wt * g.z};
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          v[a] += wg[a];
-          S[3 * a] += wg[a] * di;
-          S[3 * a + 1] += wg[a] * dj;
-          S[3 * a + 2] += wg[a] * dk;
-        }
-      }
-    }
-  }
-  float cc = 4.0f * p.inv_dx;  // coef * dx = 4/dx
-#pragma unroll
-  for (int q = 0; q < 9; ++q) C[q] = S[q] * cc;
+  g2p_gather(p, global_vel(p), b, f, w, v, C);
 }
 
 __device__ __forceinline__ void advect(const Params& p, float x[3], const float v[3]) {
@@ -96,59 +157,88 @@ __device__ __forceinline__ void advect(const Params& p, float x[3], const float 
   }
 }
 
-// Scatter one particle's (momentum, mass) stencil.  TILE_MODE: into the smem
-// tile with origin `org`; else straight into gm with REDG.F32x4.
+// Per-particle P2G payload, computed in pass 1 of the fused kernel and kept
+// in registers across the tile's scale reduction.
+struct Payload {
+  int b[3];      // base cell of the (advected) position
+  float f[3];    // fractional offset in cells
+  float m;       // mass
+  float mv[3];   // m v
+  float A[9];    // m C + k P F^T (kernels.py:264-275)
+};
+
+constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: FFMA -> round-to-nearest int in the low bits
+constexpr int MAGIC_BITS = 0x4B400000;
+
+__device__ __forceinline__ int fixq(float wt, float val) {
+  return __float_as_int(fmaf(wt, val, MAGIC)) - MAGIC_BITS;
+}
+
+// Scatter one payload.  TILE_MODE: int32 fixed-point ATOMS.ADD into the smem
+// tile (origin org, per-channel scale S); else float REDG.F32x4 into gm.
 template <bool TILE_MODE>
-__device__ __forceinline__ void p2g_scatter(const Params& p, float* tile, const int org[3],
-                                            const int b[3], const float f[3], const float w[3][3],
-                                            float m, const float mv[3], const float A[9]) {
-  float ax[3][3], ay[3][3], az[3][3];  // A[:,axis] * dp(axis, offset)
+__device__ __forceinline__ void p2g_scatter(const Params& p, int* tile, const int org[3],
+                                            const Payload& q, const float S[4]) {
+  float w[3][3];
+  float dxs[3][3];  // (offset - f) * dx
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    float d0 = ((float)q - f[0]) * p.dx, d1 = ((float)q - f[1]) * p.dx, d2 = ((float)q - f[2]) * p.dx;
+  for (int a = 0; a < 3; ++a) {
+    float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
+    w[a][0] = 0.5f * (t0 * t0);
+    w[a][1] = 0.75f - t1 * t1;
+    w[a][2] = 0.5f * (t2 * t2);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * p.dx;
+  }
+  // scaled payload: channel r of (mv, m) in tile units
+  const float sc[4] = {TILE_MODE ? S[0] : 1.f, TILE_MODE ? S[1] : 1.f, TILE_MODE ? S[2] : 1.f,
+                       TILE_MODE ? S[3] : 1.f};
+  float ax[3][3], ay[3][3], az[3][3];
+#pragma unroll
+  for (int o = 0; o < 3; ++o)
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      ax[q][r] = A[3 * r] * d0;
-      ay[q][r] = A[3 * r + 1] * d1;
-      az[q][r] = A[3 * r + 2] * d2;
+      ax[o][r] = q.A[3 * r] * sc[r] * dxs[0][o];
+      ay[o][r] = q.A[3 * r + 1] * sc[r] * dxs[1][o];
+      az[o][r] = q.A[3 * r + 2] * sc[r] * dxs[2][o];
     }
-  }
+  const float mvs[3] = {q.mv[0] * sc[0], q.mv[1] * sc[1], q.mv[2] * sc[2]};
+  const float ms = q.m * sc[3];
   int ox[3], oy[3], oz[3];
   if (TILE_MODE) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      ox[q] = (b[0] - org[0] + q) * TILE * TILE;
-      oy[q] = (b[1] - org[1] + q) * TILE;
-      oz[q] = (b[2] - org[2] + q);
+    for (int o = 0; o < 3; ++o) {
+      ox[o] = (q.b[0] - org[0] + o) * TILE * TILE;
+      oy[o] = (q.b[1] - org[1] + o) * TILE;
+      oz[o] = (q.b[2] - org[2] + o);
     }
   } else {
-    axis_offsets(b[0], p.nb[1] * p.nb[2] * 64, 16, ox);
-    axis_offsets(b[1], p.nb[2] * 64, 4, oy);
-    axis_offsets(b[2], 64, 1, oz);
+    axis_offsets(q.b[0], p.nb[1] * p.nb[2] * 64, 16, ox);
+    axis_offsets(q.b[1], p.nb[2] * 64, 4, oy);
+    axis_offsets(q.b[2], 64, 1, oz);
   }
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      float wij = w[0][i] * w[1][j];
+      const float wij = w[0][i] * w[1][j];
       float bij[3];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) bij[r] = mv[r] + ax[i][r] + ay[j][r];
-      int oij = ox[i] + oy[j];
+      for (int r = 0; r < 3; ++r) bij[r] = mvs[r] + ax[i][r] + ay[j][r];
+      const int oij = ox[i] + oy[j];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float wt = wij * w[2][k];
-        int idx = oij + oz[k];
-        float4 c = make_float4(wt * (bij[0] + az[k][0]), wt * (bij[1] + az[k][1]),
-                               wt * (bij[2] + az[k][2]), wt * m);
+        const float wt = wij * w[2][k];
+        const int idx = oij + oz[k];
         if (TILE_MODE) {
-          float* t = tile + 4 * idx;
-          atomicAdd(t, c.x);
-          atomicAdd(t + 1, c.y);
-          atomicAdd(t + 2, c.z);
-          atomicAdd(t + 3, c.w);
+          int* t = tile + idx;  // SoA channels: conflict-free banks for spread nodes
+          atomicAdd(t, fixq(wt, bij[0] + az[k][0]));
+          atomicAdd(t + TILE_NODES, fixq(wt, bij[1] + az[k][1]));
+          atomicAdd(t + 2 * TILE_NODES, fixq(wt, bij[2] + az[k][2]));
+          atomicAdd(t + 3 * TILE_NODES, fixq(wt, ms));
         } else {
-          atomicAdd(p.gm + idx, c);
+          atomicAdd(p.gm + idx, make_float4(wt * (bij[0] + az[k][0]), wt * (bij[1] + az[k][1]),
+                                            wt * (bij[2] + az[k][2]), wt * ms));
           mark_brick(p, idx);
         }
       }
@@ -156,84 +246,363 @@ __device__ __forceinline__ void p2g_scatter(const Params& p, float* tile, const 
   }
 }
 
-template <bool G2P, bool P2G>
-__global__ void __launch_bounds__(256) fused_kernel(Params p) {
-  extern __shared__ float4 tile4[];
-  float* tile = reinterpret_cast<float*>(tile4);
+// Pass 1 for one particle slot: (G2P + advect) or (load v, C), then F update
+// + stress -> payload.  STORE: write x and F back.  Returns det(F').
+template <bool G2P, bool STORE = true>
+__device__ __forceinline__ float particle_payload(const Params& p, long long i, Payload& q,
+                                                  const TileVel* tv = nullptr) {
+  float x[3] = {ldf(p, FX, i), ldf(p, FX + 1, i), ldf(p, FX + 2, i)};
+  float v[3], C[9];
+  if (G2P) {
+    int b[3];
+    float f[3], w[3][3];
+    bool in_tile = tv != nullptr;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      stencil(x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
+      if (tv) in_tile &= (b[a] - tv->org[a] >= tv->lo[a]) && (b[a] - tv->org[a] <= tv->hi[a]);
+    }
+    if (in_tile)
+      g2p_gather(p, *tv, b, f, w, v, C);
+    else
+      g2p_gather(p, global_vel(p), b, f, w, v, C);
+    advect(p, x, v);
+    if (STORE) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) stf(p, FX + a, i, x[a]);
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[a] = ldf(p, FV + a, i);
+#pragma unroll
+    for (int r = 0; r < 9; ++r) C[r] = ldf(p, FC + r, i);
+  }
+  float F[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) F[r] = ldf(p, FF + r, i);
+  const float m = ldf(p, FMASS, i), vol = ldf(p, FVOL, i);
+  const int mid = p.mat[i];
+  const float det = affine_update<false>(F, C, m, vol, __ldg(p.mu + mid), __ldg(p.lam + mid), p.dt,
+                                         p.stress_coef, p.stress_form, q.A);
+  if (STORE) {
+#pragma unroll
+    for (int r = 0; r < 9; ++r) stf(p, FF + r, i, F[r]);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float g = x[a] * p.inv_dx;
+    int bb = (int)floorf(g - 0.5f);
+    bb = max(0, min(bb, p.res[a] - 3));
+    q.b[a] = bb;
+    q.f[a] = g - (float)bb;
+    q.mv[a] = m * v[a];
+  }
+  q.m = m;
+  return det;
+}
+
+// Per-channel magnitude bound of a payload's node contributions / weight:
+// |mv_r + (A dp)_r| <= |mv_r| + 1.5 dx sum_c |A_rc|, and m.
+__device__ __forceinline__ void payload_bound(const Params& p, const Payload& q, float b[4]) {
+  const float h = 1.5f * p.dx;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    b[r] = fabsf(q.mv[r]) + h * (fabsf(q.A[3 * r]) + fabsf(q.A[3 * r + 1]) + fabsf(q.A[3 * r + 2]));
+  b[3] = q.m;
+}
+
+// Fixed-point scale of one channel for a work item of n particles whose
+// per-particle bound is B: S = 2^floor(log2(min(2^22, 2^31 / n) / (W B))), with
+// W = 0.4219 the largest 27-point weight.  Then every contribution fits the
+// FFMA magic-number conversion (|c S| < 2^22) and no node sum of the item
+// can leave int32 (n * W * B * S <= 2^31).
+__device__ __forceinline__ float channel_scale(float B, int n) {
+  if (!(B > 0.f)) return 1.0f;
+  const float lim = fminf(4194304.0f, 2147483648.0f / (float)max(n, 1));
+  return exp2f(floorf(log2f(lim / (0.4219f * B))));
+}
+
+__device__ __forceinline__ void block_max4(float mx[4], unsigned (*warp_max)[FUSED_THREADS / 32],
+                                           float out[4]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(mx[c]));
+    if (lane == 0) warp_max[c][wid] = u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    unsigned u = 0;
+#pragma unroll
+    for (int w = 0; w < FUSED_THREADS / 32; ++w) u = max(u, warp_max[c][w]);
+    out[c] = __uint_as_float(u);
+  }
+}
+
+// Stage A of a substep: G2P(n) -> advect -> F update -> Neo-Hookean stress for
+// every particle of a work item; writes x, F and the P2G payload (m v, A:
+// 12 floats SoA) and the item's exact per-channel bound.  No shared-memory
+// tile, so occupancy is set by registers alone (latency hiding for the
+// 27-node gathers).  G2P=false: first substep of a stretch (v, C from memory).
+template <bool G2P>
+__global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, float* __restrict__ pay,
+                                                                    float4* __restrict__ bounds,
+                                                                    const int* __restrict__ item_box) {
+  extern __shared__ float vtile[];  // G2P: 3 x TILE_NODES SoA velocity tile of the item
+  __shared__ unsigned warp_max[4][FUSED_THREADS / 32];
   const int nwork = *p.nwork;
   unsigned inverted = 0;
   for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
     const int4 item = p.work[wi];
-    int bin = item.x;
-    int bz = bin % p.nbin[2];
-    int by = (bin / p.nbin[2]) % p.nbin[1];
-    int bx = bin / (p.nbin[1] * p.nbin[2]);
-    const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
-    if (P2G) {
-      for (int t = threadIdx.x; t < TILE_NODES; t += blockDim.x) tile4[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncthreads();
-    }
-    for (int i = item.y + threadIdx.x; i < item.z; i += blockDim.x) {
-      float x[3] = {ldf(p, FX, i), ldf(p, FX + 1, i), ldf(p, FX + 2, i)};
-      float v[3], C[9];
-      if (G2P) {
-        g2p_gather(p, x, v, C);
-        advect(p, x, v);
+    TileVel tv;
+    tv.t = vtile;
+    if (G2P) {
+      const int bin = item.x;
+      const int bz = bin % p.nbin[2];
+      const int by = (bin / p.nbin[2]) % p.nbin[1];
+      const int bx = bin / (p.nbin[1] * p.nbin[2]);
+      tv.org[0] = bx * BIN - MARGIN;
+      tv.org[1] = by * BIN - MARGIN;
+      tv.org[2] = bz * BIN - MARGIN;
+      // the base cells this item scattered from in the previous substep's P2G are
+      // exactly the ones it gathers from now (x is unchanged in between)
+      const int pb = item_box[wi];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) stf(p, FX + a, i, x[a]);
-        if (!P2G) {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) stf(p, FV + a, i, v[a]);
-#pragma unroll
-          for (int q = 0; q < 9; ++q) stf(p, FC + q, i, C[q]);
+      for (int a = 0; a < 3; ++a) {
+        tv.lo[a] = (pb >> (4 * a)) & 15;
+        tv.hi[a] = (pb >> (12 + 4 * a)) & 15;
+      }
+      // 2-D mapping over the (y, z) node box, loop along x
+      const int ty = tv.lo[1] + (threadIdx.x >> 4), tz = tv.lo[2] + (threadIdx.x & 15);
+      const int gj = tv.org[1] + ty, gk = tv.org[2] + tz;
+      if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
+        const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                             ((gj & 3) << 2) + (gk & 3);
+        const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+        for (int tx = tv.lo[0]; tx <= tv.hi[0] + 2; ++tx) {
+          const int gi = tv.org[0] + tx;
+          const float4 g = __ldg(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
+          const int t = (tx * TILE + ty) * TILE + tz;
+          vtile[t] = g.x;
+          vtile[TILE_NODES + t] = g.y;
+          vtile[2 * TILE_NODES + t] = g.z;
         }
-      } else {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) v[a] = ldf(p, FV + a, i);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) C[q] = ldf(p, FC + q, i);
       }
-      if (P2G) {
-        float F[9], A[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) F[q] = ldf(p, FF + q, i);
-        float m = ldf(p, FMASS, i), vol = ldf(p, FVOL, i);
-        int mid = p.mat[i];
-        float det = affine_update<false>(F, C, m, vol, __ldg(p.mu + mid), __ldg(p.lam + mid), p.dt,
-                                         p.stress_coef, p.stress_form, A);
-        inverted += det <= 0.0f;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) stf(p, FF + q, i, F[q]);
-        int b[3];
-        float f[3], w[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) stencil(x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
-        float mv[3] = {m * v[0], m * v[1], m * v[2]};
-        bool inside = true;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) inside &= (b[a] - org[a] >= 0) && (b[a] - org[a] <= TILE - 3);
-        if (inside)
-          p2g_scatter<true>(p, tile, org, b, f, w, m, mv, A);
-        else
-          p2g_scatter<false>(p, tile, org, b, f, w, m, mv, A);
-      }
+      __syncthreads();
     }
-    if (P2G) {
-      __syncthreads();
-      for (int t = threadIdx.x; t < TILE_NODES; t += blockDim.x) {
-        float4 a = tile4[t];
-        if (a.x == 0.f && a.y == 0.f && a.z == 0.f && a.w == 0.f) continue;
-        int tz = t % TILE, ty = (t / TILE) % TILE, tx = t / (TILE * TILE);
-        int gi = org[0] + tx, gj = org[1] + ty, gk = org[2] + tz;
-        if (gi < 0 || gj < 0 || gk < 0 || gi >= p.res[0] || gj >= p.res[1] || gk >= p.res[2]) continue;
-        long long idx = node_index(gi, gj, gk, p.nb[1], p.nb[2]);
-        atomicAdd(p.gm + idx, a);
-        mark_brick(p, idx);
+    float mx[4] = {0.f, 0.f, 0.f, 0.f};
+    for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
+      Payload q;
+      const float det = particle_payload<G2P>(p, i, q, G2P ? &tv : nullptr);
+      inverted += det <= 0.0f;
+      float b[4];
+      payload_bound(p, q, b);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mx[c] = fmaxf(mx[c], b[c]);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) pay[r * p.cap + i] = q.mv[r];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) pay[(3 + r) * p.cap + i] = q.A[r];
+    }
+    float out[4];
+    block_max4(mx, warp_max, out);
+    if (threadIdx.x == 0) bounds[wi] = make_float4(out[0], out[1], out[2], out[3]);
+    __syncthreads();
+  }
+  warp_count_add(p.inverted, inverted);
+}
+
+// Tile scatter of one payload with lane-rotated channels.  All four channels
+// are written in the uniform form wt * (b_q + (A_q dp)) (mass: b = m, A row =
+// 0), and in atomic slot s lane l writes channel (s + l) & 3: up to four lanes
+// of the same cell (the common case in cell-sorted order) then target four
+// different channel arrays, i.e. different addresses and banks, in every
+// ATOMS instead of serializing on one address.
+__device__ __forceinline__ void p2g_scatter_rot(const Params& p, int* tile, const int org[3],
+                                                const Payload& q, const float S[4], int rot) {
+  float w[3][3], dxs[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
+    w[a][0] = 0.5f * (t0 * t0);
+    w[a][1] = 0.75f - t1 * t1;
+    w[a][2] = 0.5f * (t2 * t2);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * p.dx;
+  }
+  // rotated, scaled channel rows: slot s <- channel (s + rot) & 3
+  float b[4], A[4][3];
+  int off[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int ch = (s + rot) & 3;
+    const float sc = ch == 0 ? S[0] : ch == 1 ? S[1] : ch == 2 ? S[2] : S[3];
+    const float bv = ch == 0 ? q.mv[0] : ch == 1 ? q.mv[1] : ch == 2 ? q.mv[2] : q.m;
+    b[s] = bv * sc;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float av = ch == 0 ? q.A[c] : ch == 1 ? q.A[3 + c] : ch == 2 ? q.A[6 + c] : 0.0f;
+      A[s][c] = av * sc;
+    }
+    off[s] = ch * TILE_NODES;
+  }
+  float ax[3][4], ay[3][4], az[3][4];
+#pragma unroll
+  for (int o = 0; o < 3; ++o)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      ax[o][s] = A[s][0] * dxs[0][o];
+      ay[o][s] = A[s][1] * dxs[1][o];
+      az[o][s] = A[s][2] * dxs[2][o];
+    }
+  const int base = ((q.b[0] - org[0]) * TILE + (q.b[1] - org[1])) * TILE + (q.b[2] - org[2]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float wij = w[0][i] * w[1][j];
+      float bij[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) bij[s] = b[s] + ax[i][s] + ay[j][s];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float wt = wij * w[2][k];
+        int* t = tile + base + (i * TILE + j) * TILE + k;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) atomicAdd(t + off[s], fixq(wt, bij[s] + az[k][s]));
       }
-      __syncthreads();
     }
   }
-  if (P2G) warp_count_add(p.inverted, inverted);
+}
+
+// Stage B: P2G of one work item (<= CHUNK particles, cell-sorted) into an int32
+// fixed-point shared-memory tile (fp32 atomicAdd on shared memory is a CAS loop
+// on sm_100a; int32 ATOMS.ADD is native).  Each channel's power-of-two scale
+// comes from the item's exact bound (channel_scale: no contribution leaves the
+// FFMA magic range and no node sum can leave int32).  Particles whose stencil
+// leaves the tile go straight to gm with float REDG.F32x4.  The flush walks
+// only the touched node box, rescales exactly, issues one REDG.F32x4 per
+// non-empty node, re-zeroes the tile, marks each touched 4^3 brick active once
+// and records the box for the next substep's G2P tile.
+__global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(Params p, const float* __restrict__ pay,
+                                                                               const float4* __restrict__ bounds,
+                                                                               int* __restrict__ item_box) {
+  extern __shared__ int tile[];  // SoA: 4 x TILE_NODES int32 channels (mv x, y, z, m)
+  __shared__ int touched[TILE_BRICKS * TILE_BRICKS * TILE_BRICKS];
+  __shared__ int box[6];
+  __shared__ float scale_s[4];
+  const int nwork = *p.nwork;
+  for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
+  for (int t = threadIdx.x; t < TILE_BRICKS * TILE_BRICKS * TILE_BRICKS; t += blockDim.x) touched[t] = 0;
+  if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
+  const int rot = threadIdx.x & 3;
+  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const int4 item = p.work[wi];
+    const int bin = item.x;
+    const int bz = bin % p.nbin[2];
+    const int by = (bin / p.nbin[2]) % p.nbin[1];
+    const int bx = bin / (p.nbin[1] * p.nbin[2]);
+    const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
+    if (threadIdx.x < 4) {
+      const float4 bd = bounds[wi];
+      const float bc[4] = {bd.x, bd.y, bd.z, bd.w};
+      scale_s[threadIdx.x] = channel_scale(bc[threadIdx.x], item.z - item.y);
+    }
+    __syncthreads();
+    const float S[4] = {scale_s[0], scale_s[1], scale_s[2], scale_s[3]};
+    int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
+    for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
+      Payload q;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) q.mv[r] = pay[r * p.cap + i];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) q.A[r] = pay[(3 + r) * p.cap + i];
+      q.m = ldf(p, FMASS, i);
+      bool fits = true;
+      int lc[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float g = ldf(p, FX + a, i) * p.inv_dx;
+        int bb = (int)floorf(g - 0.5f);
+        bb = max(0, min(bb, p.res[a] - 3));
+        q.b[a] = bb;
+        q.f[a] = g - (float)bb;
+        lc[a] = bb - org[a];
+        fits &= (lc[a] >= 0) && (lc[a] <= TILE - 3);
+      }
+      if (fits) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lo_c[a] = min(lo_c[a], lc[a]);
+          hi_c[a] = max(hi_c[a], lc[a]);
+        }
+        p2g_scatter_rot(p, tile, org, q, S, rot);
+      } else {
+        const float one[4] = {1.f, 1.f, 1.f, 1.f};
+        p2g_scatter<false>(p, tile, org, q, one);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int l = __reduce_min_sync(0xffffffffu, lo_c[a]);
+      const int h = __reduce_max_sync(0xffffffffu, hi_c[a]);
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(&box[a], l);
+        atomicMax(&box[3 + a], h);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // empty box (all particles fell back to gm) encodes lo = 15 > hi
+      const bool empty = box[3] < box[0];
+      item_box[wi] = empty ? 0x00000FFF
+                           : (box[0] | (box[1] << 4) | (box[2] << 8) | (box[3] << 12) | (box[4] << 16) | (box[5] << 20));
+    }
+    const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
+    {
+      // 2-D mapping: thread -> (ty, tz) column of the box, loop over tx
+      const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
+      for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+        const int tz = z0 + (c & 15), ty = y0 + (c >> 4);
+        const int gj = org[1] + ty, gk = org[2] + tz;
+        if (tz > z1 || ty > y1 || x1 < x0 || gj < 0 || gk < 0 || gj >= p.res[1] || gk >= p.res[2]) continue;
+        const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                             ((gj & 3) << 2) + (gk & 3);
+        const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+        const int lby = (gj >> BRICK_SHIFT) - (org[1] >> BRICK_SHIFT);
+        const int lbz = (gk >> BRICK_SHIFT) - (org[2] >> BRICK_SHIFT);
+        for (int tx = x0; tx <= x1; ++tx) {
+          const int t = (tx * TILE + ty) * TILE + tz;
+          const int4 a = make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t],
+                                   tile[3 * TILE_NODES + t]);
+          if ((a.x | a.y | a.z | a.w) == 0) continue;
+          tile[t] = 0;
+          tile[TILE_NODES + t] = 0;
+          tile[2 * TILE_NODES + t] = 0;
+          tile[3 * TILE_NODES + t] = 0;
+          const int gi = org[0] + tx;
+          if (gi < 0 || gi >= p.res[0]) continue;
+          const long long idx = (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4);
+          atomicAdd(p.gm + idx, make_float4((float)a.x * inv[0], (float)a.y * inv[1],
+                                            (float)a.z * inv[2], (float)a.w * inv[3]));
+          const int lbx = (gi >> BRICK_SHIFT) - (org[0] >> BRICK_SHIFT);
+          touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz] = 1;
+        }
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < TILE_BRICKS * TILE_BRICKS * TILE_BRICKS; t += blockDim.x) {
+      if (!touched[t]) continue;
+      touched[t] = 0;
+      const int lbz = t % TILE_BRICKS, lby = (t / TILE_BRICKS) % TILE_BRICKS, lbx = t / (TILE_BRICKS * TILE_BRICKS);
+      const long long b = ((long long)((org[0] >> BRICK_SHIFT) + lbx) * p.nb[1] + ((org[1] >> BRICK_SHIFT) + lby)) *
+                              p.nb[2] + ((org[2] >> BRICK_SHIFT) + lbz);
+      mark_brick(p, b << 6);
+    }
+    if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
+    __syncthreads();
+  }
 }
 
 // Final G2P of a frame / stage g2p_advect: thread per particle.
@@ -328,33 +697,94 @@ __global__ void reset_counter_kernel(int* c, int* c2) {
 // binning (counting sort by 8^3-cell bin)
 // ---------------------------------------------------------------------------
 
-__global__ void bin_key_kernel(Params p, int* key, int* rank, int* bin_count) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
+// Re-binning = counting sort of particle slots by (8^3-cell bin, local cell):
+// bin_key (warp-aggregated counters) -> scan -> bin_fill -> bin_local_sort
+// (per-bin counting sort over the 512 local cells in shared memory) ->
+// gather_permute (coalesced writes).  Lanes of a warp then share cells, so
+// shared-memory tile reads broadcast and int atomics hit few banks.
+__global__ void bin_key_kernel(Params p, int* key, int* lcell, int* rank, int* bin_count) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool valid = i < p.n;
+  const unsigned mask = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
   int c[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     float g = ldf(p, FX + a, i) * p.inv_dx;
     int bb = (int)floorf(g - 0.5f);
-    c[a] = max(0, min(bb, p.res[a] - 3)) >> BIN_SHIFT;
+    c[a] = max(0, min(bb, p.res[a] - 3));
   }
-  int k = (c[0] * p.nbin[1] + c[1]) * p.nbin[2] + c[2];
+  const int k = ((c[0] >> BIN_SHIFT) * p.nbin[1] + (c[1] >> BIN_SHIFT)) * p.nbin[2] + (c[2] >> BIN_SHIFT);
   key[i] = k;
-  rank[i] = atomicAdd(bin_count + k, 1);
+  lcell[i] = (((c[0] & (BIN - 1)) * BIN) + (c[1] & (BIN - 1))) * BIN + (c[2] & (BIN - 1));
+  const unsigned peers = __match_any_sync(mask, k);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(bin_count + k, __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  rank[i] = base + __popc(peers & ((1u << lane) - 1u));
 }
 
-__global__ void permute_kernel(const float* __restrict__ src, const int* __restrict__ src_mat,
-                               const int* __restrict__ src_orig, float* __restrict__ dst,
-                               int* __restrict__ dst_mat, int* __restrict__ dst_orig,
-                               const int* __restrict__ key, const int* __restrict__ rank,
-                               const int* __restrict__ start, long long n, long long cap) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void bin_fill_kernel(const int* key, const int* lcell, const int* rank, const int* start,
+                                int* sidx, int* slc, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  long long d = (long long)start[key[i]] + rank[i];
+  const int d = start[key[i]] + rank[i];
+  sidx[d] = (int)i;
+  slc[d] = lcell[i];
+}
+
+constexpr int LOCAL_CELLS = BIN * BIN * BIN;
+
+// One CTA per bin (grid-stride): counting sort of the bin's slots by local cell.
+__global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_count, const int* bin_start,
+                                                             int nbins, const int* sidx, const int* slc,
+                                                             int* rk, int* perm) {
+  __shared__ int cnt[LOCAL_CELLS];
+  __shared__ int wsum[8];
+  for (int b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int nb = bin_count[b];
+    if (nb == 0) continue;
+    const int s = bin_start[b];
+    for (int c = threadIdx.x; c < LOCAL_CELLS; c += blockDim.x) cnt[c] = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb; e += blockDim.x) rk[s + e] = atomicAdd(&cnt[slc[s + e]], 1);
+    __syncthreads();
+    // exclusive scan of 512 counters: 2 per thread
+    const int c0 = cnt[2 * threadIdx.x], c1 = cnt[2 * threadIdx.x + 1];
+    int incl = c0 + c1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int f = 0; f < NF; ++f) dst[f * cap + d] = src[f * cap + i];
-  dst_mat[d] = src_mat[i];
-  dst_orig[d] = src_orig[i];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int woff = 0;
+    for (int w = 0; w < wid; ++w) woff += wsum[w];
+    const int excl = woff + incl - c0 - c1;
+    __syncthreads();
+    cnt[2 * threadIdx.x] = excl;
+    cnt[2 * threadIdx.x + 1] = excl + c0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb; e += blockDim.x) perm[s + cnt[slc[s + e]] + rk[s + e]] = sidx[s + e];
+    __syncthreads();
+  }
+}
+
+__global__ void gather_permute_kernel(const float* __restrict__ src, const int* __restrict__ src_mat,
+                                      const int* __restrict__ src_orig, float* __restrict__ dst,
+                                      int* __restrict__ dst_mat, int* __restrict__ dst_orig,
+                                      const int* __restrict__ perm, long long n, long long cap) {
+  const long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const long long s = perm[d];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) dst[f * cap + d] = __ldg(src + f * cap + s);
+  dst_mat[d] = __ldg(src_mat + s);
+  dst_orig[d] = __ldg(src_orig + s);
 }
 
 __global__ void make_work_kernel(const int* bin_count, const int* bin_start, int nbins, int4* work,

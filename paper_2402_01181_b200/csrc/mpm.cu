@@ -45,6 +45,11 @@ struct mpm_ctx {
   int cur = 0;
   int* key = nullptr;
   int* rank = nullptr;
+  int* lcell = nullptr;  // local cell in bin
+  int* sidx = nullptr;   // slots grouped by bin
+  int* slc = nullptr;    // their local cells
+  int* bperm = nullptr;  // final (bin, cell) order -> source slot
+  int* item_box = nullptr;
 
   // bins
   int nbin[3] = {0, 0, 0};
@@ -52,6 +57,8 @@ struct mpm_ctx {
   int* bin_count = nullptr;
   int* bin_start = nullptr;
   int4* work = nullptr;
+  float4* item_bounds = nullptr;
+  float* pay = nullptr;  // stage A -> stage B payload, NPAY x cap
   long long work_cap = 0;
   std::vector<int*> scan_tmp;  // per level block sums (two per level)
   std::vector<long long> scan_len;
@@ -89,7 +96,7 @@ struct mpm_ctx {
   struct Mark { int kind; cudaEvent_t a, b; };
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> event_pool;
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -149,7 +156,7 @@ cudaEvent_t pool_event(mpm_ctx* ctx) {
   return e;
 }
 
-// kind: 0 fused, 1 grid op, 2 rebin, 3 g2p
+// kind: 0 stage A (g2p_stress), 1 grid op, 2 rebin, 3 g2p, 4 stage B (p2g_tile)
 struct TimedRegion {
   mpm_ctx* ctx;
   int kind;
@@ -343,13 +350,20 @@ int rebin(mpm_ctx* ctx) {
   Params p = make_params(ctx);
   CK(cudaMemsetAsync(ctx->bin_count, 0, sizeof(int) * ctx->nbins, ctx->stream));
   CK(cudaMemsetAsync(ctx->counters + 1, 0, sizeof(int), ctx->stream));
-  bin_key_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p, ctx->key, ctx->rank, ctx->bin_count);
+  bin_key_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(p, ctx->key, ctx->lcell, ctx->rank,
+                                                                     ctx->bin_count);
   LAUNCHED();
   TRY(scan_exclusive(ctx, ctx->bin_count, ctx->bin_start, ctx->nbins));
+  bin_fill_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(ctx->key, ctx->lcell, ctx->rank, ctx->bin_start,
+                                                                     ctx->sidx, ctx->slc, ctx->n);
+  LAUNCHED();
+  bin_local_sort_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(ctx->bin_count, ctx->bin_start, ctx->nbins,
+                                                                ctx->sidx, ctx->slc, ctx->rank, ctx->bperm);
+  LAUNCHED();
   int nxt = ctx->cur ^ 1;
-  permute_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
+  gather_permute_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
       ctx->P[ctx->cur], ctx->mat[ctx->cur], ctx->orig[ctx->cur], ctx->P[nxt], ctx->mat[nxt], ctx->orig[nxt],
-      ctx->key, ctx->rank, ctx->bin_start, ctx->n, ctx->cap);
+      ctx->bperm, ctx->n, ctx->cap);
   LAUNCHED();
   ctx->cur = nxt;
   make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(ctx->bin_count, ctx->bin_start,
@@ -360,14 +374,24 @@ int rebin(mpm_ctx* ctx) {
 
 int launch_fused(mpm_ctx* ctx, bool g2p) {
   Params p = make_params(ctx);
-  size_t smem = sizeof(float4) * TILE_NODES;
+  size_t smem = sizeof(int) * 4 * TILE_NODES;
   CK(cudaMemsetAsync(ctx->counters, 0, sizeof(int), ctx->stream));
-  TimedRegion tr(ctx, 0);
-  if (g2p)
-    fused_kernel<true, true><<<ctx->fused_blocks, 256, smem, ctx->stream>>>(p);
-  else
-    fused_kernel<false, true><<<ctx->fused_blocks, 256, smem, ctx->stream>>>(p);
-  LAUNCHED();
+  {
+    TimedRegion tr(ctx, 0);
+    if (g2p)
+      g2p_stress_kernel<true><<<ctx->sms * 3, FUSED_THREADS, sizeof(float) * 3 * TILE_NODES, ctx->stream>>>(
+          p, ctx->pay, ctx->item_bounds, ctx->item_box);
+    else
+      g2p_stress_kernel<false><<<ctx->sms * 8, FUSED_THREADS, 0, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
+                                                                               ctx->item_box);
+    LAUNCHED();
+  }
+  {
+    TimedRegion tr(ctx, 4);
+    p2g_tile_kernel<<<ctx->fused_blocks, P2G_THREADS, smem, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
+                                                                          ctx->item_box);
+    LAUNCHED();
+  }
   return 0;
 }
 
@@ -484,11 +508,12 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
   if (!rc) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
-    size_t smem = sizeof(float4) * TILE_NODES;
-    cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    size_t smem = sizeof(int) * 4 * TILE_NODES;
+    cudaFuncSetAttribute(g2p_stress_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * 3 * TILE_NODES));
+    cudaFuncSetAttribute(p2g_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<true, true>, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p2g_tile_kernel, P2G_THREADS, smem);
     ctx->fused_blocks = ctx->sms * std::max(1, occ);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   }
@@ -504,7 +529,7 @@ int mpm_destroy(mpm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1],
+  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box,
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
                   ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag};
@@ -575,8 +600,15 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
     }
     TRY(dalloc(ctx, &ctx->key, (size_t)cap));
     TRY(dalloc(ctx, &ctx->rank, (size_t)cap));
+    TRY(dalloc(ctx, &ctx->lcell, (size_t)cap));
+    TRY(dalloc(ctx, &ctx->sidx, (size_t)cap));
+    TRY(dalloc(ctx, &ctx->slc, (size_t)cap));
+    TRY(dalloc(ctx, &ctx->bperm, (size_t)cap));
     ctx->work_cap = ctx->nbins + cap / CHUNK + 1;
     TRY(dalloc(ctx, &ctx->work, (size_t)ctx->work_cap));
+    TRY(dalloc(ctx, &ctx->item_bounds, (size_t)ctx->work_cap));
+    TRY(dalloc(ctx, &ctx->pay, (size_t)cap * NPAY));
+    TRY(dalloc(ctx, &ctx->item_box, (size_t)ctx->work_cap));
     if (ctx->perm) {
       cudaFree(ctx->perm);
       cudaFree(ctx->payload);
@@ -900,6 +932,8 @@ int mpm_get_timing(mpm_ctx* ctx, double* out) {
   CK(cudaStreamSynchronize(ctx->stream));
   out[8] = h[0];
   out[9] = h[1];
+  out[10] = ctx->acc[8];
+  out[11] = ctx->acc[9];
   for (double& a : ctx->acc) a = 0.0;
   return 0;
 }
