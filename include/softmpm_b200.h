@@ -129,10 +129,11 @@ int mpm_collision_field(mpm_ctx *ctx, double theta, double *dist, int32_t *obj);
 int mpm_has_nan(mpm_ctx *ctx, int *flag);
 /* Per-kernel CUDA-event timing on the context stream (bench/roofline).
  * When enabled every fast-path launch is bracketed by events; mpm_get_timing
- * fills out[12] = {g2p_stress_ms, g2p_stress_launches, grid_op_ms,
+ * fills out[14] = {g2p_stress_ms, g2p_stress_launches, grid_op_ms,
  * grid_op_launches, rebin_ms, rebin_calls, g2p_ms, g2p_launches,
- * active_bricks_last, work_items_last, p2g_tile_ms, p2g_tile_launches}
- * accumulated since the last enable, and resets them. */
+ * active_bricks_last, work_items_last, p2g_tile_ms, p2g_tile_launches,
+ * fused_ms, fused_launches} accumulated since the last enable, and resets
+ * them. */
 int mpm_set_timing(mpm_ctx *ctx, int enable);
 int mpm_get_timing(mpm_ctx *ctx, double *out);
 /* Kernel launches issued by this context so far (evidence counter). */

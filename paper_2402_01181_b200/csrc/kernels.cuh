@@ -246,12 +246,39 @@ __device__ __forceinline__ void p2g_scatter(const Params& p, int* tile, const in
   }
 }
 
-// Pass 1 for one particle slot: (G2P + advect) or (load v, C), then F update
+// Raw particle fields of one slot.
+template <bool G2P>
+struct PRaw {
+  float x[3];
+  float F[9];
+  float m, vol;
+  int mid;
+  float v[G2P ? 1 : 3];
+  float C[G2P ? 1 : 9];
+};
+
+template <bool G2P>
+__device__ __forceinline__ void load_raw(const Params& p, long long i, PRaw<G2P>& r) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) r.x[a] = ldf(p, FX + a, i);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) r.F[q] = ldf(p, FF + q, i);
+  r.m = ldf(p, FMASS, i);
+  r.vol = ldf(p, FVOL, i);
+  r.mid = p.mat[i];
+  if (!G2P) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) r.v[a] = ldf(p, FV + a, i);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) r.C[q] = ldf(p, FC + q, i);
+  }
+}
+
+// Stage-A work for one slot: (G2P + advect) or (v, C as loaded), then F update
 // + stress -> payload.  STORE: write x and F back.  Returns det(F').
 template <bool G2P, bool STORE = true>
-__device__ __forceinline__ float particle_payload(const Params& p, long long i, Payload& q,
-                                                  const TileVel* tv = nullptr) {
-  float x[3] = {ldf(p, FX, i), ldf(p, FX + 1, i), ldf(p, FX + 2, i)};
+__device__ __forceinline__ float compute_payload(const Params& p, long long i, PRaw<G2P>& r, Payload& q,
+                                                 const TileVel* tv) {
   float v[3], C[9];
   if (G2P) {
     int b[3];
@@ -259,45 +286,40 @@ __device__ __forceinline__ float particle_payload(const Params& p, long long i, 
     bool in_tile = tv != nullptr;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      stencil(x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
+      stencil(r.x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
       if (tv) in_tile &= (b[a] - tv->org[a] >= tv->lo[a]) && (b[a] - tv->org[a] <= tv->hi[a]);
     }
     if (in_tile)
       g2p_gather(p, *tv, b, f, w, v, C);
     else
       g2p_gather(p, global_vel(p), b, f, w, v, C);
-    advect(p, x, v);
+    advect(p, r.x, v);
     if (STORE) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) stf(p, FX + a, i, x[a]);
+      for (int a = 0; a < 3; ++a) stf(p, FX + a, i, r.x[a]);
     }
   } else {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) v[a] = ldf(p, FV + a, i);
+    for (int a = 0; a < 3; ++a) v[a] = r.v[a];
 #pragma unroll
-    for (int r = 0; r < 9; ++r) C[r] = ldf(p, FC + r, i);
+    for (int c = 0; c < 9; ++c) C[c] = r.C[c];
   }
-  float F[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) F[r] = ldf(p, FF + r, i);
-  const float m = ldf(p, FMASS, i), vol = ldf(p, FVOL, i);
-  const int mid = p.mat[i];
-  const float det = affine_update<false>(F, C, m, vol, __ldg(p.mu + mid), __ldg(p.lam + mid), p.dt,
+  const float det = affine_update<false>(r.F, C, r.m, r.vol, __ldg(p.mu + r.mid), __ldg(p.lam + r.mid), p.dt,
                                          p.stress_coef, p.stress_form, q.A);
   if (STORE) {
 #pragma unroll
-    for (int r = 0; r < 9; ++r) stf(p, FF + r, i, F[r]);
+    for (int c = 0; c < 9; ++c) stf(p, FF + c, i, r.F[c]);
   }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    float g = x[a] * p.inv_dx;
+    const float g = r.x[a] * p.inv_dx;
     int bb = (int)floorf(g - 0.5f);
     bb = max(0, min(bb, p.res[a] - 3));
     q.b[a] = bb;
     q.f[a] = g - (float)bb;
-    q.mv[a] = m * v[a];
+    q.mv[a] = r.m * v[a];
   }
-  q.m = m;
+  q.m = r.m;
   return det;
 }
 
@@ -322,40 +344,26 @@ __device__ __forceinline__ float channel_scale(float B, int n) {
   return exp2f(floorf(log2f(lim / (0.4219f * B))));
 }
 
-__device__ __forceinline__ void block_max4(float mx[4], unsigned (*warp_max)[FUSED_THREADS / 32],
-                                           float out[4]) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(mx[c]));
-    if (lane == 0) warp_max[c][wid] = u;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    unsigned u = 0;
-#pragma unroll
-    for (int w = 0; w < FUSED_THREADS / 32; ++w) u = max(u, warp_max[c][w]);
-    out[c] = __uint_as_float(u);
-  }
-}
-
 // Stage A of a substep: G2P(n) -> advect -> F update -> Neo-Hookean stress for
-// every particle of a work item; writes x, F and the P2G payload (m v, A:
-// 12 floats SoA) and the item's exact per-channel bound.  No shared-memory
-// tile, so occupancy is set by registers alone (latency hiding for the
-// 27-node gathers).  G2P=false: first substep of a stretch (v, C from memory).
+// every particle of a work item; writes x, F and the P2G payload (m v, A, m:
+// NPAY floats SoA) and the item's exact per-channel bound (warp max ->
+// atomicMax on the float bits; bounds are zeroed before the launch).  The G2P
+// reads a double-buffered shared-memory SoA velocity tile covering the node
+// box this item scattered to in the previous substep (x is unchanged in
+// between), so each item costs one barrier.
+// G2P=false: first substep of a stretch (v, C from memory).
 template <bool G2P>
 __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, float* __restrict__ pay,
                                                                     float4* __restrict__ bounds,
                                                                     const int* __restrict__ item_box) {
-  extern __shared__ float vtile[];  // G2P: 3 x TILE_NODES SoA velocity tile of the item
-  __shared__ unsigned warp_max[4][FUSED_THREADS / 32];
+  extern __shared__ float vtiles[];  // G2P: 2 x (3 x TILE_NODES) SoA velocity tiles
   const int nwork = *p.nwork;
   unsigned inverted = 0;
-  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+  int buf = 0;
+  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, buf ^= 1) {
     const int4 item = p.work[wi];
     TileVel tv;
+    float* vtile = vtiles + buf * 3 * TILE_NODES;
     tv.t = vtile;
     if (G2P) {
       const int bin = item.x;
@@ -365,8 +373,6 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
       tv.org[0] = bx * BIN - MARGIN;
       tv.org[1] = by * BIN - MARGIN;
       tv.org[2] = bz * BIN - MARGIN;
-      // the base cells this item scattered from in the previous substep's P2G are
-      // exactly the ones it gathers from now (x is unchanged in between)
       const int pb = item_box[wi];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -393,8 +399,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
     }
     float mx[4] = {0.f, 0.f, 0.f, 0.f};
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
+      PRaw<G2P> cur;
+      load_raw<G2P>(p, i, cur);
       Payload q;
-      const float det = particle_payload<G2P>(p, i, q, G2P ? &tv : nullptr);
+      const float det = compute_payload<G2P>(p, i, cur, q, G2P ? &tv : nullptr);
       inverted += det <= 0.0f;
       float b[4];
       payload_bound(p, q, b);
@@ -404,73 +412,87 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
       for (int r = 0; r < 3; ++r) pay[r * p.cap + i] = q.mv[r];
 #pragma unroll
       for (int r = 0; r < 9; ++r) pay[(3 + r) * p.cap + i] = q.A[r];
+      pay[12 * p.cap + i] = q.m;
     }
-    float out[4];
-    block_max4(mx, warp_max, out);
-    if (threadIdx.x == 0) bounds[wi] = make_float4(out[0], out[1], out[2], out[3]);
-    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(mx[c]));
+      if ((threadIdx.x & 31) == 0 && u) atomicMax(reinterpret_cast<unsigned*>(bounds + wi) + c, u);
+    }
   }
   warp_count_add(p.inverted, inverted);
 }
 
-// Tile scatter of one payload with lane-rotated channels.  All four channels
-// are written in the uniform form wt * (b_q + (A_q dp)) (mass: b = m, A row =
-// 0), and in atomic slot s lane l writes channel (s + l) & 3: up to four lanes
-// of the same cell (the common case in cell-sorted order) then target four
-// different channel arrays, i.e. different addresses and banks, in every
-// ATOMS instead of serializing on one address.
+// Per-thread rotated view of the payload rows: in atomic slot s lane l
+// writes channel (s + l) & 3 (0..2 = m v components, 3 = mass).  Every
+// channel is written in the uniform form wt * (b + A_row . dp) (mass: b = m,
+// A row = 0), so up to four lanes of the same cell -- the common case in
+// cell-sorted order -- target four different channel arrays (different
+// addresses and banks) in every ATOMS instead of serializing on one address.
+struct RotRows {
+  const float* b[4];  // pay row of b for slot s
+  const float* a[4];  // first pay row of the A row for slot s
+  float amul[4];      // 1, or 0 for the mass slot
+  int off[4];         // channel offset in the SoA tile
+  int ch[4];
+};
+
+__device__ __forceinline__ RotRows make_rot_rows(const Params& p, const float* pay, int rot) {
+  RotRows rr;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int ch = (s + rot) & 3;
+    rr.ch[s] = ch;
+    rr.b[s] = pay + (long long)(ch < 3 ? ch : 12) * p.cap;
+    rr.a[s] = pay + (long long)(ch < 3 ? 3 + 3 * ch : 3) * p.cap;
+    rr.amul[s] = ch < 3 ? 1.0f : 0.0f;
+    rr.off[s] = ch * TILE_NODES;
+  }
+  return rr;
+}
+
+// Tile scatter of particle i (base cell b, fraction f) with rotated rows.
 __device__ __forceinline__ void p2g_scatter_rot(const Params& p, int* tile, const int org[3],
-                                                const Payload& q, const float S[4], int rot) {
+                                                const RotRows& rr, const float sc[4], long long i,
+                                                const int b[3], const float f[3]) {
   float w[3][3], dxs[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
+    const float t0 = 1.5f - f[a], t1 = f[a] - 1.0f, t2 = f[a] - 0.5f;
     w[a][0] = 0.5f * (t0 * t0);
     w[a][1] = 0.75f - t1 * t1;
     w[a][2] = 0.5f * (t2 * t2);
 #pragma unroll
-    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * p.dx;
+    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - f[a]) * p.dx;
   }
-  // rotated, scaled channel rows: slot s <- channel (s + rot) & 3
-  float b[4], A[4][3];
-  int off[4];
+  float bs[4], ax[3][4], ay[3][4], az[3][4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    const int ch = (s + rot) & 3;
-    const float sc = ch == 0 ? S[0] : ch == 1 ? S[1] : ch == 2 ? S[2] : S[3];
-    const float bv = ch == 0 ? q.mv[0] : ch == 1 ? q.mv[1] : ch == 2 ? q.mv[2] : q.m;
-    b[s] = bv * sc;
+    bs[s] = rr.b[s][i] * sc[s];
+    const float sa = sc[s] * rr.amul[s];
+    const float a0 = rr.a[s][i] * sa, a1 = rr.a[s][p.cap + i] * sa, a2 = rr.a[s][2 * p.cap + i] * sa;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float av = ch == 0 ? q.A[c] : ch == 1 ? q.A[3 + c] : ch == 2 ? q.A[6 + c] : 0.0f;
-      A[s][c] = av * sc;
+    for (int o = 0; o < 3; ++o) {
+      ax[o][s] = a0 * dxs[0][o];
+      ay[o][s] = a1 * dxs[1][o];
+      az[o][s] = a2 * dxs[2][o];
     }
-    off[s] = ch * TILE_NODES;
   }
-  float ax[3][4], ay[3][4], az[3][4];
+  const int base = ((b[0] - org[0]) * TILE + (b[1] - org[1])) * TILE + (b[2] - org[2]);
 #pragma unroll
-  for (int o = 0; o < 3; ++o)
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      ax[o][s] = A[s][0] * dxs[0][o];
-      ay[o][s] = A[s][1] * dxs[1][o];
-      az[o][s] = A[s][2] * dxs[2][o];
-    }
-  const int base = ((q.b[0] - org[0]) * TILE + (q.b[1] - org[1])) * TILE + (q.b[2] - org[2]);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
+  for (int ii = 0; ii < 3; ++ii) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const float wij = w[0][i] * w[1][j];
+      const float wij = w[0][ii] * w[1][j];
       float bij[4];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) bij[s] = b[s] + ax[i][s] + ay[j][s];
+      for (int s = 0; s < 4; ++s) bij[s] = bs[s] + ax[ii][s] + ay[j][s];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float wt = wij * w[2][k];
-        int* t = tile + base + (i * TILE + j) * TILE + k;
+        int* t = tile + base + (ii * TILE + j) * TILE + k;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) atomicAdd(t + off[s], fixq(wt, bij[s] + az[k][s]));
+        for (int s = 0; s < 4; ++s) atomicAdd(t + rr.off[s], fixq(wt, bij[s] + az[k][s]));
       }
     }
   }
@@ -484,50 +506,55 @@ __device__ __forceinline__ void p2g_scatter_rot(const Params& p, int* tile, cons
 // leaves the tile go straight to gm with float REDG.F32x4.  The flush walks
 // only the touched node box, rescales exactly, issues one REDG.F32x4 per
 // non-empty node, re-zeroes the tile, marks each touched 4^3 brick active once
-// and records the box for the next substep's G2P tile.
+// (first toucher via a shared flag) and records the box for the next
+// substep's G2P tile.  Two barriers per item.
 __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(Params p, const float* __restrict__ pay,
                                                                                const float4* __restrict__ bounds,
                                                                                int* __restrict__ item_box) {
   extern __shared__ int tile[];  // SoA: 4 x TILE_NODES int32 channels (mv x, y, z, m)
-  __shared__ int touched[TILE_BRICKS * TILE_BRICKS * TILE_BRICKS];
-  __shared__ int box[6];
-  __shared__ float scale_s[4];
+  constexpr int NTB = TILE_BRICKS * TILE_BRICKS * TILE_BRICKS;
+  __shared__ int touched[NTB];
+  __shared__ int boxes[2][6];  // double-buffered by item parity: reset one while the other is live
   const int nwork = *p.nwork;
   for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
-  for (int t = threadIdx.x; t < TILE_BRICKS * TILE_BRICKS * TILE_BRICKS; t += blockDim.x) touched[t] = 0;
-  if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
-  const int rot = threadIdx.x & 3;
-  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+  if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
+  const RotRows rr = make_rot_rows(p, pay, threadIdx.x & 3);
+  int par = 0;
+  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, par ^= 1) {
+    int* box = boxes[par];
     const int4 item = p.work[wi];
     const int bin = item.x;
     const int bz = bin % p.nbin[2];
     const int by = (bin / p.nbin[2]) % p.nbin[1];
     const int bx = bin / (p.nbin[1] * p.nbin[2]);
     const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
-    if (threadIdx.x < 4) {
+    float S[4];
+    {
       const float4 bd = bounds[wi];
-      const float bc[4] = {bd.x, bd.y, bd.z, bd.w};
-      scale_s[threadIdx.x] = channel_scale(bc[threadIdx.x], item.z - item.y);
+      const int n_item = item.z - item.y;
+      S[0] = channel_scale(bd.x, n_item);
+      S[1] = channel_scale(bd.y, n_item);
+      S[2] = channel_scale(bd.z, n_item);
+      S[3] = channel_scale(bd.w, n_item);
     }
-    __syncthreads();
-    const float S[4] = {scale_s[0], scale_s[1], scale_s[2], scale_s[3]};
+    float sc[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) sc[s] = rr.ch[s] == 0 ? S[0] : rr.ch[s] == 1 ? S[1] : rr.ch[s] == 2 ? S[2] : S[3];
+    // previous item's brick flags and box (its flush ended before the last barrier)
+    for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
+    if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
     int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
-      Payload q;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) q.mv[r] = pay[r * p.cap + i];
-#pragma unroll
-      for (int r = 0; r < 9; ++r) q.A[r] = pay[(3 + r) * p.cap + i];
-      q.m = ldf(p, FMASS, i);
+      int b[3], lc[3];
+      float f[3];
       bool fits = true;
-      int lc[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const float g = ldf(p, FX + a, i) * p.inv_dx;
         int bb = (int)floorf(g - 0.5f);
         bb = max(0, min(bb, p.res[a] - 3));
-        q.b[a] = bb;
-        q.f[a] = g - (float)bb;
+        b[a] = bb;
+        f[a] = g - (float)bb;
         lc[a] = bb - org[a];
         fits &= (lc[a] >= 0) && (lc[a] <= TILE - 3);
       }
@@ -537,8 +564,18 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
           lo_c[a] = min(lo_c[a], lc[a]);
           hi_c[a] = max(hi_c[a], lc[a]);
         }
-        p2g_scatter_rot(p, tile, org, q, S, rot);
+        p2g_scatter_rot(p, tile, org, rr, sc, i, b, f);
       } else {
+        Payload q;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          q.b[a] = b[a];
+          q.f[a] = f[a];
+          q.mv[a] = pay[a * p.cap + i];
+        }
+#pragma unroll
+        for (int r = 0; r < 9; ++r) q.A[r] = pay[(3 + r) * p.cap + i];
+        q.m = pay[12 * p.cap + i];
         const float one[4] = {1.f, 1.f, 1.f, 1.f};
         p2g_scatter<false>(p, tile, org, q, one);
       }
@@ -553,56 +590,257 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
       }
     }
     __syncthreads();
+    const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
     if (threadIdx.x == 0) {
       // empty box (all particles fell back to gm) encodes lo = 15 > hi
-      const bool empty = box[3] < box[0];
-      item_box[wi] = empty ? 0x00000FFF
-                           : (box[0] | (box[1] << 4) | (box[2] << 8) | (box[3] << 12) | (box[4] << 16) | (box[5] << 20));
+      item_box[wi] = x1 - 2 < x0 ? 0x00000FFF
+                                 : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
     }
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
-    {
-      // 2-D mapping: thread -> (ty, tz) column of the box, loop over tx
-      const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
-      for (int c = threadIdx.x; c < 256; c += blockDim.x) {
-        const int tz = z0 + (c & 15), ty = y0 + (c >> 4);
-        const int gj = org[1] + ty, gk = org[2] + tz;
-        if (tz > z1 || ty > y1 || x1 < x0 || gj < 0 || gk < 0 || gj >= p.res[1] || gk >= p.res[2]) continue;
-        const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
-                             ((gj & 3) << 2) + (gk & 3);
-        const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-        const int lby = (gj >> BRICK_SHIFT) - (org[1] >> BRICK_SHIFT);
-        const int lbz = (gk >> BRICK_SHIFT) - (org[2] >> BRICK_SHIFT);
-        for (int tx = x0; tx <= x1; ++tx) {
-          const int t = (tx * TILE + ty) * TILE + tz;
-          const int4 a = make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t],
-                                   tile[3 * TILE_NODES + t]);
-          if ((a.x | a.y | a.z | a.w) == 0) continue;
-          tile[t] = 0;
-          tile[TILE_NODES + t] = 0;
-          tile[2 * TILE_NODES + t] = 0;
-          tile[3 * TILE_NODES + t] = 0;
-          const int gi = org[0] + tx;
-          if (gi < 0 || gi >= p.res[0]) continue;
-          const long long idx = (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4);
-          atomicAdd(p.gm + idx, make_float4((float)a.x * inv[0], (float)a.y * inv[1],
-                                            (float)a.z * inv[2], (float)a.w * inv[3]));
-          const int lbx = (gi >> BRICK_SHIFT) - (org[0] >> BRICK_SHIFT);
-          touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz] = 1;
-        }
+    // 2-D mapping: thread -> (ty, tz) column of the box, loop over tx
+    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+      const int tz = z0 + (c & 15), ty = y0 + (c >> 4);
+      const int gj = org[1] + ty, gk = org[2] + tz;
+      if (tz > z1 || ty > y1 || x1 - 2 < x0 || gj < 0 || gk < 0 || gj >= p.res[1] || gk >= p.res[2]) continue;
+      const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                           ((gj & 3) << 2) + (gk & 3);
+      const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+      const int lby = (gj >> BRICK_SHIFT) - (org[1] >> BRICK_SHIFT);
+      const int lbz = (gk >> BRICK_SHIFT) - (org[2] >> BRICK_SHIFT);
+      for (int tx = x0; tx <= x1; ++tx) {
+        const int t = (tx * TILE + ty) * TILE + tz;
+        const int4 a = make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t],
+                                 tile[3 * TILE_NODES + t]);
+        if ((a.x | a.y | a.z | a.w) == 0) continue;
+        tile[t] = 0;
+        tile[TILE_NODES + t] = 0;
+        tile[2 * TILE_NODES + t] = 0;
+        tile[3 * TILE_NODES + t] = 0;
+        const int gi = org[0] + tx;
+        if (gi < 0 || gi >= p.res[0]) continue;
+        const long long idx = (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4);
+        atomicAdd(p.gm + idx, make_float4((float)a.x * inv[0], (float)a.y * inv[1],
+                                          (float)a.z * inv[2], (float)a.w * inv[3]));
+        const int lbx = (gi >> BRICK_SHIFT) - (org[0] >> BRICK_SHIFT);
+        if (atomicExch(&touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz], 1) == 0) mark_brick(p, idx);
       }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < TILE_BRICKS * TILE_BRICKS * TILE_BRICKS; t += blockDim.x) {
-      if (!touched[t]) continue;
-      touched[t] = 0;
-      const int lbz = t % TILE_BRICKS, lby = (t / TILE_BRICKS) % TILE_BRICKS, lbx = t / (TILE_BRICKS * TILE_BRICKS);
-      const long long b = ((long long)((org[0] >> BRICK_SHIFT) + lbx) * p.nb[1] + ((org[1] >> BRICK_SHIFT) + lby)) *
-                              p.nb[2] + ((org[2] >> BRICK_SHIFT) + lbz);
-      mark_brick(p, b << 6);
-    }
-    if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
-    __syncthreads();
   }
+}
+
+// Fused steady-state substep: G2P(n) -> advect -> F update -> stress -> P2G(n+1)
+// in one pass per work item, with no payload round trip (the per-substep
+// working set x, F, m, V0 + grid stays L2-resident).  The G2P reads the
+// shared-memory velocity tile of the node box the item scattered to in the
+// previous substep; the P2G scatters lane-rotated channels into the int32
+// fixed-point tile whose scales come from the item's bounds in the previous
+// substep (x BOUND_SAFETY for momentum, exact for mass).  A particle that
+// exceeds those bounds or leaves the tile is scattered with float REDG.F32x4
+// into gm directly.  The item's exact new bounds (bounds_out, zeroed before
+// the launch) and node box are recorded for the next substep.
+constexpr float BOUND_SAFETY = 2.0f;
+
+__device__ __forceinline__ float sel4(bool r1, bool r2, float v0, float v1, float v2, float v3) {
+  const float a = r1 ? v1 : v0;
+  const float b = r1 ? v3 : v2;
+  return r2 ? b : a;
+}
+
+__global__ void __launch_bounds__(FUSED_THREADS, 2) fused_kernel(Params p, const float4* __restrict__ bounds_in,
+                                                                 float4* __restrict__ bounds_out,
+                                                                 int* __restrict__ item_box) {
+  extern __shared__ float smem[];
+  float* vtile = smem;                                           // 3 x TILE_NODES
+  int* tile = reinterpret_cast<int*>(smem + 3 * TILE_NODES);     // 4 x TILE_NODES
+  constexpr int NTB = TILE_BRICKS * TILE_BRICKS * TILE_BRICKS;
+  __shared__ int touched[NTB];
+  __shared__ int boxes[2][6];
+  const int nwork = *p.nwork;
+  for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
+  if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
+  const int rot = threadIdx.x & 3;
+  const bool r1 = rot & 1, r2 = rot & 2;
+  int off[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) off[s] = ((s + rot) & 3) * TILE_NODES;
+  unsigned inverted = 0;
+  int par = 0;
+  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, par ^= 1) {
+    int* box = boxes[par];
+    const int4 item = p.work[wi];
+    const int bin = item.x;
+    const int bz = bin % p.nbin[2];
+    const int by = (bin / p.nbin[2]) % p.nbin[1];
+    const int bx = bin / (p.nbin[1] * p.nbin[2]);
+    const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
+    TileVel tv;
+    tv.t = vtile;
+    tv.org[0] = org[0];
+    tv.org[1] = org[1];
+    tv.org[2] = org[2];
+    {
+      const int pb = item_box[wi];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        tv.lo[a] = (pb >> (4 * a)) & 15;
+        tv.hi[a] = (pb >> (12 + 4 * a)) & 15;
+      }
+      const int ty = tv.lo[1] + (threadIdx.x >> 4), tz = tv.lo[2] + (threadIdx.x & 15);
+      const int gj = org[1] + ty, gk = org[2] + tz;
+      if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
+        const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                             ((gj & 3) << 2) + (gk & 3);
+        const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+        for (int tx = tv.lo[0]; tx <= tv.hi[0] + 2; ++tx) {
+          const int gi = org[0] + tx;
+          const float4 g = __ldg(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
+          const int t = (tx * TILE + ty) * TILE + tz;
+          vtile[t] = g.x;
+          vtile[TILE_NODES + t] = g.y;
+          vtile[2 * TILE_NODES + t] = g.z;
+        }
+      }
+    }
+    for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
+    if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
+    const int n_item = item.z - item.y;
+    float B[4], S[4];
+    {
+      const float4 bd = bounds_in[wi];
+      B[0] = bd.x * BOUND_SAFETY;
+      B[1] = bd.y * BOUND_SAFETY;
+      B[2] = bd.z * BOUND_SAFETY;
+      B[3] = bd.w;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) S[c] = channel_scale(B[c], n_item);
+    }
+    float sc[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) sc[s] = sel4(r1, r2, S[s & 3], S[(s + 1) & 3], S[(s + 2) & 3], S[(s + 3) & 3]);
+    __syncthreads();  // [1] velocity tile ready; previous flush complete
+    float mx[4] = {0.f, 0.f, 0.f, 0.f};
+    int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
+    for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
+      PRaw<true> r;
+      load_raw<true>(p, i, r);
+      Payload q;
+      const float det = compute_payload<true>(p, i, r, q, &tv);
+      inverted += det <= 0.0f;
+      float bnd[4];
+      payload_bound(p, q, bnd);
+      bool fits = true;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        mx[c] = fmaxf(mx[c], bnd[c]);
+        fits &= bnd[c] <= B[c];
+      }
+      int lc[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lc[a] = q.b[a] - org[a];
+        fits &= (lc[a] >= 0) && (lc[a] <= TILE - 3);
+      }
+      if (!fits) {
+        const float one[4] = {1.f, 1.f, 1.f, 1.f};
+        p2g_scatter<false>(p, tile, org, q, one);
+        continue;
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo_c[a] = min(lo_c[a], lc[a]);
+        hi_c[a] = max(hi_c[a], lc[a]);
+      }
+      // rotated, scaled channel rows (mass: b = m, A row = 0)
+      const float chb[4] = {q.mv[0], q.mv[1], q.mv[2], q.m};
+      float bs[4], as[4][3];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        bs[s] = sel4(r1, r2, chb[s & 3], chb[(s + 1) & 3], chb[(s + 2) & 3], chb[(s + 3) & 3]) * sc[s];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float ca[4] = {q.A[c], q.A[3 + c], q.A[6 + c], 0.0f};
+          as[s][c] = sel4(r1, r2, ca[s & 3], ca[(s + 1) & 3], ca[(s + 2) & 3], ca[(s + 3) & 3]) * sc[s];
+        }
+      }
+      float w[3][3], dxs[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
+        w[a][0] = 0.5f * (t0 * t0);
+        w[a][1] = 0.75f - t1 * t1;
+        w[a][2] = 0.5f * (t2 * t2);
+#pragma unroll
+        for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * p.dx;
+      }
+      const int base = (lc[0] * TILE + lc[1]) * TILE + lc[2];
+#pragma unroll
+      for (int ii = 0; ii < 3; ++ii) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const float wij = w[0][ii] * w[1][j];
+          float bij[4];
+#pragma unroll
+          for (int s = 0; s < 4; ++s) bij[s] = bs[s] + as[s][0] * dxs[0][ii] + as[s][1] * dxs[1][j];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float wt = wij * w[2][k];
+            int* t = tile + base + (ii * TILE + j) * TILE + k;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) atomicAdd(t + off[s], fixq(wt, bij[s] + as[s][2] * dxs[2][k]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(mx[c]));
+      if ((threadIdx.x & 31) == 0 && u) atomicMax(reinterpret_cast<unsigned*>(bounds_out + wi) + c, u);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int l = __reduce_min_sync(0xffffffffu, lo_c[a]);
+      const int h = __reduce_max_sync(0xffffffffu, hi_c[a]);
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(&box[a], l);
+        atomicMax(&box[3 + a], h);
+      }
+    }
+    __syncthreads();  // [2] scatter complete
+    const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
+    if (threadIdx.x == 0)
+      item_box[wi] = x1 - 2 < x0 ? 0x00000FFF
+                                 : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
+    const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
+    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+      const int tz = z0 + (c & 15), ty = y0 + (c >> 4);
+      const int gj = org[1] + ty, gk = org[2] + tz;
+      if (tz > z1 || ty > y1 || x1 - 2 < x0 || gj < 0 || gk < 0 || gj >= p.res[1] || gk >= p.res[2]) continue;
+      const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                           ((gj & 3) << 2) + (gk & 3);
+      const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+      const int lby = (gj >> BRICK_SHIFT) - (org[1] >> BRICK_SHIFT);
+      const int lbz = (gk >> BRICK_SHIFT) - (org[2] >> BRICK_SHIFT);
+      for (int tx = x0; tx <= x1; ++tx) {
+        const int t = (tx * TILE + ty) * TILE + tz;
+        const int4 a = make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t], tile[3 * TILE_NODES + t]);
+        if ((a.x | a.y | a.z | a.w) == 0) continue;
+        tile[t] = 0;
+        tile[TILE_NODES + t] = 0;
+        tile[2 * TILE_NODES + t] = 0;
+        tile[3 * TILE_NODES + t] = 0;
+        const int gi = org[0] + tx;
+        if (gi < 0 || gi >= p.res[0]) continue;
+        const long long idx = (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4);
+        atomicAdd(p.gm + idx, make_float4((float)a.x * inv[0], (float)a.y * inv[1], (float)a.z * inv[2],
+                                          (float)a.w * inv[3]));
+        const int lbx = (gi >> BRICK_SHIFT) - (org[0] >> BRICK_SHIFT);
+        if (atomicExch(&touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz], 1) == 0) mark_brick(p, idx);
+      }
+    }
+    __syncthreads();  // [3] flush complete: tile zero, velocity tile free
+  }
+  warp_count_add(p.inverted, inverted);
 }
 
 // Final G2P of a frame / stage g2p_advect: thread per particle.

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +59,7 @@ struct mpm_ctx {
   int* bin_start = nullptr;
   int4* work = nullptr;
   float4* item_bounds = nullptr;
+  float4* item_bounds2 = nullptr;  // fused kernel: bounds of substep n (in) / n+1 (out)
   float* pay = nullptr;  // stage A -> stage B payload, NPAY x cap
   long long work_cap = 0;
   std::vector<int*> scan_tmp;  // per level block sums (two per level)
@@ -96,7 +98,8 @@ struct mpm_ctx {
   struct Mark { int kind; cudaEvent_t a, b; };
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> event_pool;
-  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
 };
 
 namespace {
@@ -156,7 +159,7 @@ cudaEvent_t pool_event(mpm_ctx* ctx) {
   return e;
 }
 
-// kind: 0 stage A (g2p_stress), 1 grid op, 2 rebin, 3 g2p, 4 stage B (p2g_tile)
+// kind: 0 stage A (g2p_stress), 1 grid op, 2 rebin, 3 g2p, 4 stage B (p2g_tile), 5 fused
 struct TimedRegion {
   mpm_ctx* ctx;
   int kind;
@@ -372,26 +375,41 @@ int rebin(mpm_ctx* ctx) {
   return 0;
 }
 
+// One substep's particle work.  g2p=false: first substep after a re-binning
+// (v, C from memory): stage A<false> (exact bounds + payload) then stage B.
+// g2p=true: the fused steady-state kernel (bounds of the previous substep).
 int launch_fused(mpm_ctx* ctx, bool g2p) {
   Params p = make_params(ctx);
-  size_t smem = sizeof(int) * 4 * TILE_NODES;
   CK(cudaMemsetAsync(ctx->counters, 0, sizeof(int), ctx->stream));
-  {
-    TimedRegion tr(ctx, 0);
-    if (g2p)
-      g2p_stress_kernel<true><<<ctx->sms * 3, FUSED_THREADS, sizeof(float) * 3 * TILE_NODES, ctx->stream>>>(
+  if (!g2p || ctx->split_mode) {
+    CK(cudaMemsetAsync(ctx->item_bounds, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
+    {
+      TimedRegion tr(ctx, 0);
+      if (g2p)
+        g2p_stress_kernel<true><<<ctx->sms * 3, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES, ctx->stream>>>(
+            p, ctx->pay, ctx->item_bounds, ctx->item_box);
+      else
+        g2p_stress_kernel<false><<<ctx->sms * 8, FUSED_THREADS, 0, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
+                                                                                 ctx->item_box);
+      LAUNCHED();
+    }
+    {
+      TimedRegion tr(ctx, 4);
+      p2g_tile_kernel<<<ctx->fused_blocks, P2G_THREADS, sizeof(int) * 4 * TILE_NODES, ctx->stream>>>(
           p, ctx->pay, ctx->item_bounds, ctx->item_box);
-    else
-      g2p_stress_kernel<false><<<ctx->sms * 8, FUSED_THREADS, 0, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
-                                                                               ctx->item_box);
-    LAUNCHED();
+      LAUNCHED();
+    }
+    return 0;
   }
+  // fused: bounds_in = item_bounds (last substep), bounds_out = item_bounds2, then swap
+  CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
   {
-    TimedRegion tr(ctx, 4);
-    p2g_tile_kernel<<<ctx->fused_blocks, P2G_THREADS, smem, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
-                                                                          ctx->item_box);
+    TimedRegion tr(ctx, 5);
+    fused_kernel<<<ctx->sms * 2, FUSED_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
+        p, ctx->item_bounds, ctx->item_bounds2, ctx->item_box);
     LAUNCHED();
   }
+  std::swap(ctx->item_bounds, ctx->item_bounds2);
   return 0;
 }
 
@@ -509,8 +527,14 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
     size_t smem = sizeof(int) * 4 * TILE_NODES;
+    cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * 7 * TILE_NODES));
+    {
+      const char* e = getenv("SOFTMPM_SPLIT");
+      ctx->split_mode = e && e[0] == '1';
+    }
     cudaFuncSetAttribute(g2p_stress_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * 3 * TILE_NODES));
+                         (int)(sizeof(float) * 6 * TILE_NODES));
     cudaFuncSetAttribute(p2g_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p2g_tile_kernel, P2G_THREADS, smem);
@@ -529,7 +553,7 @@ int mpm_destroy(mpm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box,
+  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box,
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
                   ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag};
@@ -607,6 +631,7 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
     ctx->work_cap = ctx->nbins + cap / CHUNK + 1;
     TRY(dalloc(ctx, &ctx->work, (size_t)ctx->work_cap));
     TRY(dalloc(ctx, &ctx->item_bounds, (size_t)ctx->work_cap));
+    TRY(dalloc(ctx, &ctx->item_bounds2, (size_t)ctx->work_cap));
     TRY(dalloc(ctx, &ctx->pay, (size_t)cap * NPAY));
     TRY(dalloc(ctx, &ctx->item_box, (size_t)ctx->work_cap));
     if (ctx->perm) {
@@ -934,6 +959,8 @@ int mpm_get_timing(mpm_ctx* ctx, double* out) {
   out[9] = h[1];
   out[10] = ctx->acc[8];
   out[11] = ctx->acc[9];
+  out[12] = ctx->acc[10];
+  out[13] = ctx->acc[11];
   for (double& a : ctx->acc) a = 0.0;
   return 0;
 }
