@@ -333,15 +333,18 @@ __device__ __forceinline__ void payload_bound(const Params& p, const Payload& q,
   b[3] = q.m;
 }
 
-// Fixed-point scale of one channel for a work item of n particles whose
-// per-particle bound is B: S = 2^floor(log2(min(2^22, 2^31 / n) / (W B))), with
-// W = 0.4219 the largest 27-point weight.  Then every contribution fits the
-// FFMA magic-number conversion (|c S| < 2^22) and no node sum of the item
-// can leave int32 (n * W * B * S <= 2^31).
-__device__ __forceinline__ float channel_scale(float B, int n) {
+// Fixed-point scale of one channel for a work item whose per-particle bound
+// is B and whose densest cell held maxcnt particles at re-binning:
+//   S = 2^floor(log2(min(2^22 / (W B), 2^31 / (K * 2 maxcnt * B)))),
+// W = 0.4219 the largest 27-point weight, K = 1.75^3 = 5.36 the sum over the 27
+// stencil offsets of each offset's largest weight.  Every contribution then
+// fits the FFMA magic-number conversion (|c S| < 2^22), and a node sum --
+// at most K * (particles per cell) * B -- stays inside int32 even if cells
+// double their occupancy before the next re-binning.
+__device__ __forceinline__ float channel_scale(float B, int maxcnt) {
   if (!(B > 0.f)) return 1.0f;
-  const float lim = fminf(4194304.0f, 2147483648.0f / (float)max(n, 1));
-  return exp2f(floorf(log2f(lim / (0.4219f * B))));
+  const float lim = fminf(4194304.0f / 0.4219f, 2147483648.0f / (5.36f * 2.0f * (float)max(maxcnt, 1)));
+  return exp2f(floorf(log2f(lim / B)));
 }
 
 // Stage A of a substep: G2P(n) -> advect -> F update -> Neo-Hookean stress for
@@ -515,6 +518,7 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
   constexpr int NTB = TILE_BRICKS * TILE_BRICKS * TILE_BRICKS;
   __shared__ int touched[NTB];
   __shared__ int boxes[2][6];  // double-buffered by item parity: reset one while the other is live
+  __shared__ float scale_s[4];
   const int nwork = *p.nwork;
   for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
@@ -528,21 +532,19 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
     const int by = (bin / p.nbin[2]) % p.nbin[1];
     const int bx = bin / (p.nbin[1] * p.nbin[2]);
     const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
-    float S[4];
-    {
-      const float4 bd = bounds[wi];
-      const int n_item = item.z - item.y;
-      S[0] = channel_scale(bd.x, n_item);
-      S[1] = channel_scale(bd.y, n_item);
-      S[2] = channel_scale(bd.z, n_item);
-      S[3] = channel_scale(bd.w, n_item);
-    }
-    float sc[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) sc[s] = rr.ch[s] == 0 ? S[0] : rr.ch[s] == 1 ? S[1] : rr.ch[s] == 2 ? S[2] : S[3];
     // previous item's brick flags and box (its flush ended before the last barrier)
     for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
+    if (threadIdx.x < 4) {
+      const float4 bd = bounds[wi];
+      const float bc[4] = {bd.x, bd.y, bd.z, bd.w};
+      scale_s[threadIdx.x] = channel_scale(bc[threadIdx.x], item.w);
+    }
+    __syncthreads();
+    const float S[4] = {scale_s[0], scale_s[1], scale_s[2], scale_s[3]};
+    float sc[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) sc[s] = rr.ch[s] == 0 ? S[0] : rr.ch[s] == 1 ? S[1] : rr.ch[s] == 2 ? S[2] : S[3];
     int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
       int b[3], lc[3];
@@ -656,6 +658,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) fused_kernel(Params p, const
   constexpr int NTB = TILE_BRICKS * TILE_BRICKS * TILE_BRICKS;
   __shared__ int touched[NTB];
   __shared__ int boxes[2][6];
+  __shared__ float scale_s[2][4];
   const int nwork = *p.nwork;
   for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
@@ -704,21 +707,20 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) fused_kernel(Params p, const
     }
     for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
-    const int n_item = item.z - item.y;
-    float B[4], S[4];
+    float B[4];
     {
       const float4 bd = bounds_in[wi];
       B[0] = bd.x * BOUND_SAFETY;
       B[1] = bd.y * BOUND_SAFETY;
       B[2] = bd.z * BOUND_SAFETY;
       B[3] = bd.w;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) S[c] = channel_scale(B[c], n_item);
     }
+    if (threadIdx.x < 4) scale_s[par][threadIdx.x] = channel_scale(B[threadIdx.x], item.w);
+    __syncthreads();  // [1] velocity tile + scales ready; previous flush complete
+    const float S[4] = {scale_s[par][0], scale_s[par][1], scale_s[par][2], scale_s[par][3]};
     float sc[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s) sc[s] = sel4(r1, r2, S[s & 3], S[(s + 1) & 3], S[(s + 2) & 3], S[(s + 3) & 3]);
-    __syncthreads();  // [1] velocity tile ready; previous flush complete
     float mx[4] = {0.f, 0.f, 0.f, 0.f};
     int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
@@ -978,9 +980,10 @@ constexpr int LOCAL_CELLS = BIN * BIN * BIN;
 // One CTA per bin (grid-stride): counting sort of the bin's slots by local cell.
 __global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_count, const int* bin_start,
                                                              int nbins, const int* sidx, const int* slc,
-                                                             int* rk, int* perm) {
+                                                             int* rk, int* perm, int* bin_maxcnt) {
   __shared__ int cnt[LOCAL_CELLS];
   __shared__ int wsum[8];
+  __shared__ int wmax[8];
   for (int b = blockIdx.x; b < nbins; b += gridDim.x) {
     const int nb = bin_count[b];
     if (nb == 0) continue;
@@ -989,10 +992,12 @@ __global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_coun
     __syncthreads();
     for (int e = threadIdx.x; e < nb; e += blockDim.x) rk[s + e] = atomicAdd(&cnt[slc[s + e]], 1);
     __syncthreads();
-    // exclusive scan of 512 counters: 2 per thread
+    // exclusive scan of 512 counters: 2 per thread (and the densest cell)
     const int c0 = cnt[2 * threadIdx.x], c1 = cnt[2 * threadIdx.x + 1];
     int incl = c0 + c1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int cm = __reduce_max_sync(0xffffffffu, max(c0, c1));
+    if (lane == 0) wmax[wid] = cm;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -1002,6 +1007,11 @@ __global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_coun
     __syncthreads();
     int woff = 0;
     for (int w = 0; w < wid; ++w) woff += wsum[w];
+    if (threadIdx.x == 0) {
+      int mm = 0;
+      for (int w = 0; w < 8; ++w) mm = max(mm, wmax[w]);
+      bin_maxcnt[b] = mm;
+    }
     const int excl = woff + incl - c0 - c1;
     __syncthreads();
     cnt[2 * threadIdx.x] = excl;
@@ -1025,17 +1035,18 @@ __global__ void gather_permute_kernel(const float* __restrict__ src, const int* 
   dst_orig[d] = __ldg(src_orig + s);
 }
 
-__global__ void make_work_kernel(const int* bin_count, const int* bin_start, int nbins, int4* work,
-                                 int* nwork) {
+__global__ void make_work_kernel(const int* bin_count, const int* bin_start, const int* bin_maxcnt, int nbins,
+                                 int4* work, int* nwork) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nbins) return;
-  int c = bin_count[b];
+  const int c = bin_count[b];
   if (!c) return;
-  int items = (c + CHUNK - 1) / CHUNK;
-  int base = atomicAdd(nwork, items);
-  int s = bin_start[b];
+  const int items = (c + CHUNK - 1) / CHUNK;
+  const int per = (c + items - 1) / items;  // equal splits (no tiny tail item)
+  const int base = atomicAdd(nwork, items);
+  const int s = bin_start[b];
   for (int t = 0; t < items; ++t)
-    work[base + t] = make_int4(b, s + t * CHUNK, min(s + (t + 1) * CHUNK, s + c), 0);
+    work[base + t] = make_int4(b, s + t * per, min(s + (t + 1) * per, s + c), bin_maxcnt[b]);
 }
 
 // ---------------------------------------------------------------------------

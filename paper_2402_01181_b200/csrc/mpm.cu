@@ -57,6 +57,7 @@ struct mpm_ctx {
   int nbins = 0;
   int* bin_count = nullptr;
   int* bin_start = nullptr;
+  int* bin_maxcnt = nullptr;
   int4* work = nullptr;
   float4* item_bounds = nullptr;
   float4* item_bounds2 = nullptr;  // fused kernel: bounds of substep n (in) / n+1 (out)
@@ -278,6 +279,7 @@ int alloc_grid(mpm_ctx* ctx) {
   ctx->nbins = ctx->nbin[0] * ctx->nbin[1] * ctx->nbin[2];
   TRY(dalloc(ctx, &ctx->bin_count, (size_t)ctx->nbins));
   TRY(dalloc(ctx, &ctx->bin_start, (size_t)ctx->nbins));
+  TRY(dalloc(ctx, &ctx->bin_maxcnt, (size_t)ctx->nbins));
   ctx->grid_dirty = 0;
   ctx->grid_phase = 0;
   return 0;
@@ -361,7 +363,8 @@ int rebin(mpm_ctx* ctx) {
                                                                      ctx->sidx, ctx->slc, ctx->n);
   LAUNCHED();
   bin_local_sort_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(ctx->bin_count, ctx->bin_start, ctx->nbins,
-                                                                ctx->sidx, ctx->slc, ctx->rank, ctx->bperm);
+                                                                ctx->sidx, ctx->slc, ctx->rank, ctx->bperm,
+                                                                ctx->bin_maxcnt);
   LAUNCHED();
   int nxt = ctx->cur ^ 1;
   gather_permute_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
@@ -369,8 +372,8 @@ int rebin(mpm_ctx* ctx) {
       ctx->bperm, ctx->n, ctx->cap);
   LAUNCHED();
   ctx->cur = nxt;
-  make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(ctx->bin_count, ctx->bin_start,
-                                                                           ctx->nbins, ctx->work, ctx->counters + 1);
+  make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(
+      ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, ctx->counters + 1);
   LAUNCHED();
   return 0;
 }
@@ -555,7 +558,7 @@ int mpm_destroy(mpm_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box,
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
-                  ctx->bin_start, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
+                  ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
                   ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag};
   for (void* b : bufs)
     if (b) cudaFree(b);
