@@ -27,6 +27,11 @@ struct ColliderGeo {
   int sdf_res[3];
   double sdf_bmin[3];
   double sdf_ext;
+  // far-field prefilter (host-computed): box -> |half|; baked -> the smallest
+  // sampled distance on the lattice's outer layer (what any query outside
+  // the lattice box evaluates to, kernels.py:52-66 clamping)
+  float far_r;
+  float far_min;
 };
 
 struct ColliderPose {
@@ -40,6 +45,7 @@ struct ColliderPose {
 struct Colliders {
   int count;
   double theta;  // < 0: disabled
+  float theta_f;  // theta + prefilter margin (fp32)
   const ColliderGeo* geo;
   const ColliderPose* pose;  // row for this substep
   const double* sdf;
@@ -113,6 +119,36 @@ __device__ inline double world_sd(const Colliders& cs, int ci, double wx, double
   double px, py, pz;
   to_local(cs.pose[ci], wx, wy, wz, px, py, pz);
   return local_sd(cs.geo[ci], cs.sdf, px, py, pz);
+}
+
+// Conservative fp32 test: may collider ci be closer than theta_m to world
+// point (x, y, z)?  false only when the exact fp64 distance is certainly
+// >= theta (theta_m carries a margin far above fp32 rounding).
+__device__ __forceinline__ bool collider_near(const Colliders& cs, int ci, float x, float y, float z,
+                                              float theta_m) {
+  const ColliderGeo& g = cs.geo[ci];
+  const ColliderPose& q = cs.pose[ci];
+  const float d0 = x - (float)q.T[0], d1 = y - (float)q.T[1], d2 = z - (float)q.T[2];
+  if (g.kind == 0) {
+    // box SDF >= max_a (|p_a| - h_a): test the theta-inflated oriented box
+    const float px = (float)q.R[0] * d0 + (float)q.R[3] * d1 + (float)q.R[6] * d2;
+    const float py = (float)q.R[1] * d0 + (float)q.R[4] * d1 + (float)q.R[7] * d2;
+    const float pz = (float)q.R[2] * d0 + (float)q.R[5] * d1 + (float)q.R[8] * d2;
+    return fabsf(px) < (float)g.half[0] + theta_m && fabsf(py) < (float)g.half[1] + theta_m &&
+           fabsf(pz) < (float)g.half[2] + theta_m;
+  }
+  // baked: outside the lattice box the sample is >= far_min
+  if (g.far_min >= theta_m) {
+    const float px = (float)q.R[0] * d0 + (float)q.R[3] * d1 + (float)q.R[6] * d2;
+    const float py = (float)q.R[1] * d0 + (float)q.R[4] * d1 + (float)q.R[7] * d2;
+    const float pz = (float)q.R[2] * d0 + (float)q.R[5] * d1 + (float)q.R[8] * d2;
+    const float m = 1e-4f * (float)g.sdf_ext + 1e-6f;
+    const float lo0 = (float)g.sdf_bmin[0] - m, lo1 = (float)g.sdf_bmin[1] - m, lo2 = (float)g.sdf_bmin[2] - m;
+    const float e = (float)g.sdf_ext + 2.0f * m;
+    const bool inside = px >= lo0 && px <= lo0 + e && py >= lo1 && py <= lo1 + e && pz >= lo2 && pz <= lo2 + e;
+    return inside;
+  }
+  return true;
 }
 
 // Merged field at one node: min distance, ties to the lowest index, id -1

@@ -246,6 +246,7 @@ __device__ __forceinline__ void p2g_scatter(const Params& p, int* tile, const in
   }
 }
 
+
 // Raw particle fields of one slot.
 template <bool G2P>
 struct PRaw {
@@ -347,6 +348,30 @@ __device__ __forceinline__ float channel_scale(float B, int maxcnt) {
   return exp2f(floorf(log2f(lim / B)));
 }
 
+// One (ty, tz) column of the velocity tile, nodes tx in [x0, x1] (<= TILE):
+// loads issued in groups of 5 before their shared-memory stores.
+__device__ __forceinline__ void load_vtile_column(const Params& p, float* vtile, int orgx, int x0, int x1,
+                                                  int ty, int tz, long long yz, long long xstride) {
+  constexpr int G = 5;
+  for (int xs = x0; xs <= x1; xs += G) {
+    float4 g[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int gi = orgx + xs + u;
+      if (xs + u <= x1) g[u] = __ldg(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      if (xs + u <= x1) {
+        const int t = ((xs + u) * TILE + ty) * TILE + tz;
+        vtile[t] = g[u].x;
+        vtile[TILE_NODES + t] = g[u].y;
+        vtile[2 * TILE_NODES + t] = g[u].z;
+      }
+    }
+  }
+}
+
 // Stage A of a substep: G2P(n) -> advect -> F update -> Neo-Hookean stress for
 // every particle of a work item; writes x, F and the P2G payload (m v, A, m:
 // NPAY floats SoA) and the item's exact per-channel bound (warp max ->
@@ -389,14 +414,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
         const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
                              ((gj & 3) << 2) + (gk & 3);
         const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-        for (int tx = tv.lo[0]; tx <= tv.hi[0] + 2; ++tx) {
-          const int gi = tv.org[0] + tx;
-          const float4 g = __ldg(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
-          const int t = (tx * TILE + ty) * TILE + tz;
-          vtile[t] = g.x;
-          vtile[TILE_NODES + t] = g.y;
-          vtile[2 * TILE_NODES + t] = g.z;
-        }
+        load_vtile_column(p, vtile, tv.org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
       }
       __syncthreads();
     }
@@ -695,14 +713,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) fused_kernel(Params p, const
         const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
                              ((gj & 3) << 2) + (gk & 3);
         const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-        for (int tx = tv.lo[0]; tx <= tv.hi[0] + 2; ++tx) {
-          const int gi = org[0] + tx;
-          const float4 g = __ldg(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
-          const int t = (tx * TILE + ty) * TILE + tz;
-          vtile[t] = g.x;
-          vtile[TILE_NODES + t] = g.y;
-          vtile[2 * TILE_NODES + t] = g.z;
-        }
+        load_vtile_column(p, vtile, org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
       }
     }
     for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
@@ -862,58 +873,75 @@ __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
   for (int q = 0; q < 9; ++q) stf(p, FC + q, i, C[q]);
 }
 
-// Grid op (kernels.py:347-436) over active bricks (or all bricks when DENSE).
-// 64 threads per brick.  Zero-mass nodes pass momentum through unchanged
-// (kernels.py:364-365).  When `clear`, gm is zeroed for the next P2G.
+// Grid op (kernels.py:347-436) over active bricks (or all bricks when DENSE):
+// one warp per 4^3 brick, two nodes per lane (both loads in flight).
+// Zero-mass nodes pass momentum through unchanged (kernels.py:364-365).
+// Collider distances are exact fp64 (collide.cuh), but a node is only sent
+// through them when the conservative fp32 far-field bound of some collider
+// (collide.cuh: collider_far) is below theta + margin -- nodes the bound
+// clears cannot be in contact, so results are unchanged.  When `clear`, gm
+// is zeroed for the next P2G.
+__device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs, double cap, float4 a, int gi,
+                                            int gj, int gk) {
+  if (!(a.w > 0.0f) || gi >= p.res[0] || gj >= p.res[1] || gk >= p.res[2]) return a;
+  const float inv_m = 1.0f / a.w;
+  float v0 = a.x * inv_m + p.dt * p.gravity[0];
+  float v1 = a.y * inv_m + p.dt * p.gravity[1];
+  float v2 = a.z * inv_m + p.dt * p.gravity[2];
+  if (cs.theta >= 0.0 && cs.count > 0) {
+    const float fx = (float)gi * p.dx, fy = (float)gj * p.dx, fz = (float)gk * p.dx;
+    bool near = false;
+    for (int ci = 0; ci < cs.count; ++ci) near |= collider_near(cs, ci, fx, fy, fz, cs.theta_f);
+    if (near) {
+      const double wx = (double)gi * p.dx64, wy = (double)gj * p.dx64, wz = (double)gk * p.dx64;
+      double best;
+      const int ci = nearest_collider(cs, wx, wy, wz, cap, best);
+      if (best < cs.theta && ci >= 0) {
+        double vv[3] = {v0, v1, v2};
+        resolve_contact(cs, ci, wx, wy, wz, vv);
+        v0 = (float)vv[0];
+        v1 = (float)vv[1];
+        v2 = (float)vv[2];
+      }
+    }
+  }
+  const int bw = p.bwidth;
+  if (p.stick) {
+    if (gi < bw || gi >= p.res[0] - bw || gj < bw || gj >= p.res[1] - bw || gk < bw || gk >= p.res[2] - bw)
+      v0 = v1 = v2 = 0.0f;
+  } else {
+    if (gi < bw && v0 < 0.0f) v0 = 0.0f;
+    if (gi >= p.res[0] - bw && v0 > 0.0f) v0 = 0.0f;
+    if (gj < bw && v1 < 0.0f) v1 = 0.0f;
+    if (gj >= p.res[1] - bw && v1 > 0.0f) v1 = 0.0f;
+    if (gk < bw && v2 < 0.0f) v2 = 0.0f;
+    if (gk >= p.res[2] - bw && v2 > 0.0f) v2 = 0.0f;
+  }
+  return make_float4(v0, v1, v2, a.w);
+}
+
 template <bool DENSE>
 __global__ void __launch_bounds__(256) grid_op_kernel(Params p, Colliders cs, int clear) {
   const long long nitems = DENSE ? (long long)p.nb[0] * p.nb[1] * p.nb[2] : (long long)*p.active_count;
-  const int lane = threadIdx.x & 63;
-  const int li = lane >> 4, lj = (lane >> 2) & 3, lk = lane & 3;
+  const int lane = threadIdx.x & 31;
   const double cap = 2.0 * cs.theta;
-  for (long long it = (long long)blockIdx.x * (blockDim.x >> 6) + (threadIdx.x >> 6); it < nitems;
-       it += (long long)gridDim.x * (blockDim.x >> 6)) {
-    long long b = DENSE ? it : (long long)p.active_list[it];
-    int bi, bj, bk;
-    brick_coords(b, p.nb, bi, bj, bk);
-    int gi = bi * 4 + li, gj = bj * 4 + lj, gk = bk * 4 + lk;
-    long long idx = (b << 6) | lane;
-    float4 a = p.gm[idx];
-    float4 out = a;
-    if (a.w > 0.0f && gi < p.res[0] && gj < p.res[1] && gk < p.res[2]) {
-      float inv_m = 1.0f / a.w;
-      float v0 = a.x * inv_m + p.dt * p.gravity[0];
-      float v1 = a.y * inv_m + p.dt * p.gravity[1];
-      float v2 = a.z * inv_m + p.dt * p.gravity[2];
-      if (cs.theta >= 0.0 && cs.count > 0) {
-        double wx = (double)gi * p.dx64, wy = (double)gj * p.dx64, wz = (double)gk * p.dx64;
-        double best;
-        int ci = nearest_collider(cs, wx, wy, wz, cap, best);
-        if (best < cs.theta && ci >= 0) {
-          double vv[3] = {v0, v1, v2};
-          resolve_contact(cs, ci, wx, wy, wz, vv);
-          v0 = (float)vv[0];
-          v1 = (float)vv[1];
-          v2 = (float)vv[2];
-        }
-      }
-      const int bw = p.bwidth;
-      if (p.stick) {
-        if (gi < bw || gi >= p.res[0] - bw || gj < bw || gj >= p.res[1] - bw || gk < bw ||
-            gk >= p.res[2] - bw)
-          v0 = v1 = v2 = 0.0f;
-      } else {
-        if (gi < bw && v0 < 0.0f) v0 = 0.0f;
-        if (gi >= p.res[0] - bw && v0 > 0.0f) v0 = 0.0f;
-        if (gj < bw && v1 < 0.0f) v1 = 0.0f;
-        if (gj >= p.res[1] - bw && v1 > 0.0f) v1 = 0.0f;
-        if (gk < bw && v2 < 0.0f) v2 = 0.0f;
-        if (gk >= p.res[2] - bw && v2 > 0.0f) v2 = 0.0f;
-      }
-      out = make_float4(v0, v1, v2, a.w);
+  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems;
+       it += (long long)gridDim.x * (blockDim.x >> 5)) {
+    const long long b = DENSE ? it : (long long)p.active_list[it];
+    const int b32 = (int)b;
+    const int bk = b32 % p.nb[2], bj = (b32 / p.nb[2]) % p.nb[1], bi = b32 / (p.nb[2] * p.nb[1]);
+    const long long i0 = (b << 6) | lane, i1 = i0 + 32;  // local nodes lane, lane + 32
+    const float4 a0 = p.gm[i0];
+    const float4 a1 = p.gm[i1];
+    const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
+    const float4 o0 = grid_node(p, cs, cap, a0, bi * 4 + li0, bj * 4 + lj, bk * 4 + lk);
+    const float4 o1 = grid_node(p, cs, cap, a1, bi * 4 + li0 + 2, bj * 4 + lj, bk * 4 + lk);
+    p.gv[i0] = o0;
+    p.gv[i1] = o1;
+    if (clear) {
+      p.gm[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      p.gm[i1] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    p.gv[idx] = out;
-    if (clear) p.gm[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (lane == 0) p.brick_flag[b] = 0;
   }
 }

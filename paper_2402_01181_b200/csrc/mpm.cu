@@ -93,6 +93,8 @@ struct mpm_ctx {
   int* flag = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int fused_blocks = 0;
+  int gridop_blocks = 0;  // persistent grid sizes (SMs x resident CTAs)
+  int gsA_blocks = 0, gsA0_blocks = 0, clear_blocks = 0, fused_only_blocks = 0;
 
   // optional per-kernel timing: event pairs per launch, resolved lazily
   bool timing = false;
@@ -246,6 +248,8 @@ Colliders make_colliders(mpm_ctx* ctx, int row, bool use) {
   int r = ctx->pose_rows > 0 ? std::min(row, ctx->pose_rows - 1) : 0;
   cs.pose = ctx->pose ? ctx->pose + (size_t)r * std::max(ctx->ncol, 1) : nullptr;
   cs.sdf = ctx->sdf;
+  // prefilter margin: far above fp32 rounding of O(1) coordinates, far below dx
+  cs.theta_f = (float)(cs.theta + 1e-4 * ctx->cfg.dx + 1e-6);
   return cs;
 }
 
@@ -342,7 +346,7 @@ int ensure_gm_clean(mpm_ctx* ctx) {
     CK(cudaMemsetAsync(ctx->brick_flag, 0, sizeof(int) * ctx->nbricks, ctx->stream));
   } else if (ctx->grid_dirty == 1) {
     Params p = make_params(ctx);
-    clear_active_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(p);
+    clear_active_kernel<<<ctx->clear_blocks, 256, 0, ctx->stream>>>(p);
     LAUNCHED();
   }
   ctx->grid_dirty = 0;
@@ -389,10 +393,10 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
     {
       TimedRegion tr(ctx, 0);
       if (g2p)
-        g2p_stress_kernel<true><<<ctx->sms * 3, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES, ctx->stream>>>(
+        g2p_stress_kernel<true><<<ctx->gsA_blocks, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES, ctx->stream>>>(
             p, ctx->pay, ctx->item_bounds, ctx->item_box);
       else
-        g2p_stress_kernel<false><<<ctx->sms * 8, FUSED_THREADS, 0, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
+        g2p_stress_kernel<false><<<ctx->gsA0_blocks, FUSED_THREADS, 0, ctx->stream>>>(p, ctx->pay, ctx->item_bounds,
                                                                                  ctx->item_box);
       LAUNCHED();
     }
@@ -408,7 +412,7 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
   {
     TimedRegion tr(ctx, 5);
-    fused_kernel<<<ctx->sms * 2, FUSED_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
+    fused_kernel<<<ctx->fused_only_blocks, FUSED_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
         p, ctx->item_bounds, ctx->item_bounds2, ctx->item_box);
     LAUNCHED();
   }
@@ -421,9 +425,9 @@ int launch_grid_op(mpm_ctx* ctx, bool dense, bool use_col, int row, bool clear) 
   Colliders cs = make_colliders(ctx, row, use_col);
   TimedRegion tr(ctx, 1);
   if (dense)
-    grid_op_kernel<true><<<ctx->sms * 8, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
+    grid_op_kernel<true><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
   else
-    grid_op_kernel<false><<<ctx->sms * 8, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
+    grid_op_kernel<false><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
   LAUNCHED();
   return 0;
 }
@@ -542,6 +546,16 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p2g_tile_kernel, P2G_THREADS, smem);
     ctx->fused_blocks = ctx->sms * std::max(1, occ);
+    auto persistent = [&](const void* fn, int threads, size_t dyn) {
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, dyn);
+      return ctx->sms * std::max(1, o);
+    };
+    ctx->gridop_blocks = ctx->sms * 8;  // measured: more, shorter CTAs beat a persistent grid here
+    ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
+    ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
+    ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
+    ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_THREADS, sizeof(float) * 7 * TILE_NODES);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   }
   if (rc) {
@@ -770,10 +784,22 @@ int mpm_set_colliders(mpm_ctx* ctx, int count, const int32_t* kind, const double
     g.mode = mode[i];
     g.sdf_off = sdf_offset ? sdf_offset[i] : -1;
     g.sdf_ext = sdf_extent ? sdf_extent[i] : 1.0;
+    g.far_r = (float)(std::sqrt(g.half[0] * g.half[0] + g.half[1] * g.half[1] + g.half[2] * g.half[2]) * (1.0 + 1e-6));
+    g.far_min = -1.0f;
     if (g.kind == 1) {
       if (!sdf_values || g.sdf_off < 0 || g.sdf_res[0] < 2 || g.sdf_res[1] < 2 || g.sdf_res[2] < 2 ||
           g.sdf_off + (long long)g.sdf_res[0] * g.sdf_res[1] * g.sdf_res[2] > sdf_len)
         return fail(ctx, MPM_EINVAL, "baked collider: SDF lattice out of range");
+      // smallest value on the outer layer (x-fastest lattice), in metres, shaded down for fp32
+      const int rx = g.sdf_res[0], ry = g.sdf_res[1], rz = g.sdf_res[2];
+      double mn = 1e300;
+      for (int z = 0; z < rz; ++z)
+        for (int y = 0; y < ry; ++y)
+          for (int x = 0; x < rx; ++x) {
+            if (x != 0 && x != rx - 1 && y != 0 && y != ry - 1 && z != 0 && z != rz - 1) continue;
+            mn = std::min(mn, sdf_values[g.sdf_off + x + (long long)rx * (y + (long long)ry * z)]);
+          }
+      g.far_min = (float)(mn * g.sdf_ext * (mn > 0 ? 0.999999 : 1.000001));
     }
     ColliderPose& q = pose[i];
     for (int a = 0; a < 9; ++a) q.R[a] = rotation[9 * i + a];
