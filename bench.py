@@ -4,7 +4,8 @@
                     [--config c3] [--particles P] [--no-cpu-baseline]
 
 Workload (N=1): BASELINE config 3 -- a 1 M-particle Neo-Hookean slab on a
-256^3 grid pressed by a box tool moving down at 0.5 m/s (SimParams defaults:
+256^3 grid pressed 3 cm deep by a box tool moving down at 0.5 m/s, then held
+(SimParams defaults:
 dt 5e-4, 25 substeps per step, theta 0.5 dx, Coulomb mu 0.4).  One "step" is
 one ``softmpm.step`` frame = 25 substeps.  Metric: particle-substeps/s.
 
@@ -75,10 +76,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:  # sampler running before timing starts
+                time.sleep(0.01)
+            self.skip = len(self.lines)
         except Exception:
             self.proc = None
         return self
@@ -98,7 +103,8 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        lines = self.lines[getattr(self, "skip", 0):] or self.lines[-1:]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -324,7 +330,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {n} particles/GPU, {st.grid.resolution[0]}^3 grid, "
-                   f"{len(cols)} box tool(s) pressing at 0.5 m/s, 25 substeps per step",
+                   f"{len(cols)} box tool(s) pressing 3 cm at 0.5 m/s then holding, 25 substeps per step",
                    "particles_per_gpu": n, "grid": list(st.grid.resolution),
                    "substeps_per_step": nsub, "parallelism": f"replicas x{world}",
                    "l2": "flushed between steps (512 MiB memset)",
@@ -360,7 +366,7 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3"])

@@ -8,7 +8,9 @@ colliders, pose_fn).
   c1  30 K block dropped into the floor band, 64^3, no tools
   c2  30 K block, 128^3, two baked-SDF capsule jaws (grasper) on a
       down -> close -> pull keyframe path, Coulomb mu = 0.35 (sticky when closed)
-  c3  1 M slab on 256^3 pressed by a box tool moving down at 0.5 m/s
+  c3  1 M slab on 256^3 pressed 3 cm deep by a box tool moving down at 0.5 m/s,
+      then held (a deeper press at this dt exceeds the explicit CFL limit at
+      256^3 -- the CPU oracle and the GPU path blow up alike)
 """
 
 from __future__ import annotations
@@ -66,8 +68,10 @@ def c3(count: int = 1_000_000, res: int = 256, seed: int = 1):
     top = 0.1 + 0.5 * 0.0977
     half = np.array([0.08, 0.03, 0.08])
     y0 = top + half[1] + 0.005
+    press = 0.035  # 0.5 cm gap + 3 cm into the tissue
     traj = [Keyframe(0.0, [(np.array([0.5, y0, 0.5]), _Q)]),
-            Keyframe(0.2, [(np.array([0.5, y0 - 0.1, 0.5]), _Q)])]
+            Keyframe(press / 0.5, [(np.array([0.5, y0 - press, 0.5]), _Q)]),
+            Keyframe(10.0, [(np.array([0.5, y0 - press, 0.5]), _Q)])]
     cols = [RigidCollider(id=0, shape=Box(half), friction_mu=0.4)]
     pose_fn = make_pose_fn(traj)
     pose_fn(cols, 0.0)

@@ -1,0 +1,154 @@
+"""GPU scene-level parity: BASELINE configs (scaled) against the CPU oracle O1
+fed the same per-substep tool poses, plus the install() re-routing of a
+reference-shaped module."""
+import types
+from dataclasses import dataclass, field
+
+import numpy as np
+import pytest
+
+import paper_2402_01181_b200 as sm
+from paper_2402_01181_b200 import scenes
+from conftest import load_golden, rel_l2
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_for(st, mats, theta=True):
+    g = st.grid
+    return O.OracleSim(O.OracleParams(res=g.resolution, dx=g.dx, theta=0.5 * g.dx if theta else -1.0),
+                       st.x, st.v, st.F, st.C, st.mass, st.vol0, st.material_id, mats[0].mu,
+                       mats[0].lam)
+
+
+def _run_pair(st, mats, params, cols, ocols, pose_fn, frames, live=False):
+    osim = _oracle_for(st, mats)
+    packed = None
+    t = 0.0
+    for _ in range(frames):
+        sm.step(st, mats, params, cols, pose_fn)
+        for _ in range(params.substeps_per_frame):
+            pose_fn(ocols, t)
+            if packed is None or live:
+                packed = sm.pack_colliders(ocols)   # live: modes re-read every substep
+            else:
+                packed.refresh_poses(ocols)         # frozen (reference F7)
+            osim.substep(packed)
+            t += params.dt
+    return osim
+
+
+@pytest.mark.parametrize("live", [False, True])
+def test_c2_capsule_grasper_matches_oracle(live):
+    """Config 2 (scaled): baked-SDF capsule jaws go down, close (sticky) and pull."""
+    st, mats, params, cols, pose_fn = scenes.c2(count=8000, res=64, sdf_res=32)
+    _, _, _, ocols, _ = scenes.c2(count=8000, res=64, sdf_res=32)
+    params = sm.SimParams(collider_mode="live" if live else "frozen")
+    osim = _run_pair(st, mats, params, cols, ocols, pose_fn, frames=36, live=live)  # jaws close at t=0.35
+    assert st.time == pytest.approx(osim.time, rel=1e-12)
+    assert (st._collision.object_id >= 0).sum() > 0
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), getattr(osim, k)) < 1e-3, k
+    if live:
+        assert [c.mode for c in cols] == ["sticky", "sticky"]
+
+
+def test_c3_press_scaled_matches_oracle():
+    """Config 3 (scaled to 64^3): box press and hold."""
+    st, mats, params, cols, pose_fn = scenes.c3(count=60000, res=64)
+    _, _, _, ocols, _ = scenes.c3(count=60000, res=64)
+    osim = _run_pair(st, mats, params, cols, ocols, pose_fn, frames=8)
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), getattr(osim, k)) < 1e-3, k
+
+
+def test_c1_floor_drop_matches_oracle_and_rebin_interval():
+    st, mats, params, _, _ = scenes.c1(count=30000, res=64)
+    osim = _oracle_for(st, mats, theta=False)
+    for interval in (25, 5):
+        p = sm.SimParams(rebin_interval=interval)
+        sm.step(st, mats, p)
+        for _ in range(p.substeps_per_frame):
+            osim.substep(None)
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), getattr(osim, k)) < 1e-4, k
+
+
+def _fake_softmpm():
+    """A module shaped like the reference softmpm (core.SimState dataclass with
+    numpy fields, StepReport, p2g/grid_update/g2p_advect/substep/step)."""
+    core = types.ModuleType("softmpm.core")
+
+    @dataclass
+    class Grid:
+        resolution: tuple
+        extent: tuple = (1.0, 1.0, 1.0)
+
+        @property
+        def dx(self):
+            return self.extent[0] / self.resolution[0]
+
+    @dataclass
+    class StepReport:
+        step_index: int
+        sim_time: float
+        timings_ms: dict
+        inverted_particles: int
+
+    @dataclass
+    class SimState:
+        grid: Grid
+        x: np.ndarray
+        v: np.ndarray
+        F: np.ndarray
+        C: np.ndarray
+        mass: np.ndarray
+        vol0: np.ndarray
+        material_id: np.ndarray
+        time: float = 0.0
+        step_count: int = 0
+        grid_mv: np.ndarray = field(init=False)
+        grid_m: np.ndarray = field(init=False)
+
+        def __post_init__(self):
+            self.grid_mv = np.zeros(tuple(self.grid.resolution) + (3,))
+            self.grid_m = np.zeros(tuple(self.grid.resolution))
+
+    def _ref_only(*a, **k):
+        raise AssertionError("reference CPU path called after install()")
+
+    core.Grid, core.StepReport, core.SimState = Grid, StepReport, SimState
+    for nm in ("p2g", "grid_update", "g2p_advect", "substep", "step"):
+        setattr(core, nm, _ref_only)
+    mod = types.ModuleType("softmpm")
+    mod.core = core
+    for nm in ("p2g", "grid_update", "g2p_advect", "substep", "step"):
+        setattr(mod, nm, _ref_only)
+    return mod
+
+
+def test_install_reroutes_reference_shaped_module():
+    g = load_golden("floor_block.npz")
+    ref = _fake_softmpm()
+    sm.install(ref)
+    try:
+        res = tuple(int(r) for r in g["res"])
+        st = ref.core.SimState(ref.core.Grid(res), g["in_x"].copy(), g["in_v"].copy(), g["in_F"].copy(),
+                               g["in_C"].copy(), g["mass"], g["vol0"], np.zeros(len(g["in_x"]), np.int32))
+        mats = [sm.Material(float(g["E"]), float(g["nu"]), float(g["rho"]))]
+        x_obj = st.x
+        inv = ref.substep(st, mats, sm.SimParams())
+        assert inv == 0
+        assert st.x is x_obj  # results land in the caller's arrays
+        for k in ("x", "v", "F"):
+            assert rel_l2(getattr(st, k), g[f"s1_{k}"]) < 1e-5, k
+        assert st.grid_m.sum() == pytest.approx(g["mass"].sum(), rel=1e-5)
+        rep = ref.step(st, mats, sm.SimParams(substeps_per_frame=9))
+        assert isinstance(rep, ref.core.StepReport) and rep.step_index == 1
+        for k in ("x", "v", "F"):
+            assert rel_l2(getattr(st, k), g[f"s10_{k}"]) < 1e-4, k
+    finally:
+        sm.uninstall(ref)
+    with pytest.raises(AssertionError):
+        ref.step(st, mats, sm.SimParams())
