@@ -136,7 +136,12 @@ int mpm_has_nan(mpm_ctx *ctx, int *flag);
  * them. */
 int mpm_set_timing(mpm_ctx *ctx, int enable);
 int mpm_get_timing(mpm_ctx *ctx, double *out);
-/* Kernel launches issued by this context so far (evidence counter). */
+/* Runtime options: "graphs" (1 = replay fast-path frames as CUDA graphs,
+ * default), "split" (1 = stage A + stage B every substep instead of the fused
+ * kernel; A/B comparisons). */
+int mpm_set_option(mpm_ctx *ctx, const char *key, int value);
+/* Kernel launches issued by this context so far (evidence counter; a graph
+ * replay counts every kernel node it runs). */
 int64_t mpm_launch_count(mpm_ctx *ctx);
 /* Page-locked host buffer for fast uploads/downloads (e2e path). */
 void *mpm_host_alloc(int64_t bytes);

@@ -34,7 +34,7 @@ EXPORTS = (
     "mpm_particle_count", "mpm_upload_grid", "mpm_download_grid", "mpm_set_colliders",
     "mpm_set_pose_table", "mpm_p2g", "mpm_grid_update", "mpm_g2p", "mpm_substeps",
     "mpm_collision_field", "mpm_has_nan", "mpm_launch_count", "mpm_host_alloc", "mpm_host_free",
-    "mpm_set_timing", "mpm_get_timing",
+    "mpm_set_timing", "mpm_get_timing", "mpm_set_option",
 )
 
 
@@ -94,6 +94,7 @@ def lib():
     L.mpm_host_free.argtypes = [_VP]
     L.mpm_set_timing.argtypes = [_VP, ctypes.c_int]
     L.mpm_get_timing.argtypes = [_VP, _D]
+    L.mpm_set_option.argtypes = [_VP, ctypes.c_char_p, ctypes.c_int]
     _lib = L
     return L
 

@@ -30,6 +30,7 @@ constexpr int P2G_THREADS = 256;        // stage B (p2g_tile_kernel)
 constexpr int P2G_MIN_BLOCKS = 3;
 constexpr int NPAY = 13;                // payload floats per particle: m v (3), A (9), m
 constexpr int CHUNK = 4096;               // max particles per work item (larger bins split evenly)
+constexpr int MIN_CHUNK = 256;            // small scenes: items shrink to this so every SM gets work
 // 4^3 layout bricks overlapped by a tile: org = 8b - MARGIN is even, so a tile edge of TILE nodes spans
 constexpr int TILE_BRICKS = (TILE + 3 + 3) / 4;
 constexpr int NF = 26;                    // float fields per particle

@@ -1064,12 +1064,12 @@ __global__ void gather_permute_kernel(const float* __restrict__ src, const int* 
 }
 
 __global__ void make_work_kernel(const int* bin_count, const int* bin_start, const int* bin_maxcnt, int nbins,
-                                 int4* work, int* nwork) {
+                                 int4* work, int* nwork, int chunk) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nbins) return;
   const int c = bin_count[b];
   if (!c) return;
-  const int items = (c + CHUNK - 1) / CHUNK;
+  const int items = (c + chunk - 1) / chunk;
   const int per = (c + items - 1) / items;  // equal splits (no tiny tail item)
   const int base = atomicAdd(nwork, items);
   const int s = bin_start[b];

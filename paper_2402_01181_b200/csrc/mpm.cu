@@ -98,8 +98,21 @@ struct mpm_ctx {
 
   // optional per-kernel timing: event pairs per launch, resolved lazily
   bool timing = false;
-  struct Mark { int kind; cudaEvent_t a, b; };
+  struct Mark { int kind; cudaEvent_t a, b; bool graph_owned; };
   std::vector<Mark> marks;
+
+  // CUDA graphs of whole fast-path frames, keyed by the host-side start state
+  struct GraphEntry {
+    int nsub, col, cur, border, dirty, timing;
+    long long n;
+    long long kernels;  // kernel nodes in the graph (evidence counter)
+    cudaGraphExec_t exec;
+    int end_cur, end_border, end_dirty;
+    std::vector<Mark> marks;  // event nodes captured inside the graph
+  };
+  std::vector<GraphEntry> graphs;
+  bool graphs_on = true;
+  float4* bounds_a = nullptr;  // the two item-bound arrays as allocated (swap parity)
   std::vector<cudaEvent_t> event_pool;
   double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
@@ -170,15 +183,25 @@ struct TimedRegion {
   TimedRegion(mpm_ctx* c, int k) : ctx(c), kind(k) {
     if (ctx->timing) {
       a = pool_event(ctx);
-      cudaEventRecord(a, ctx->stream);
+      record(a);
     }
   }
   ~TimedRegion() {
     if (a) {
       cudaEvent_t b = pool_event(ctx);
-      cudaEventRecord(b, ctx->stream);
-      ctx->marks.push_back({kind, a, b});
+      record(b);
+      ctx->marks.push_back({kind, a, b, false});
     }
+  }
+  // inside stream capture a plain record is only a dependency marker: timing
+  // needs an event record node (cudaEventRecordExternal)
+  void record(cudaEvent_t e) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &st);
+    if (st == cudaStreamCaptureStatusActive)
+      cudaEventRecordWithFlags(e, ctx->stream, cudaEventRecordExternal);
+    else
+      cudaEventRecord(e, ctx->stream);
   }
 };
 
@@ -190,10 +213,26 @@ void resolve_marks(mpm_ctx* ctx) {
     cudaEventElapsedTime(&ms, mk.a, mk.b);
     ctx->acc[2 * mk.kind] += ms;
     ctx->acc[2 * mk.kind + 1] += 1.0;
-    ctx->event_pool.push_back(mk.a);
-    ctx->event_pool.push_back(mk.b);
+    if (!mk.graph_owned) {
+      ctx->event_pool.push_back(mk.a);
+      ctx->event_pool.push_back(mk.b);
+    }
   }
   ctx->marks.clear();
+}
+
+void invalidate_graphs(mpm_ctx* ctx) {
+  if (ctx->graphs.empty()) return;
+  cudaStreamSynchronize(ctx->stream);
+  resolve_marks(ctx);
+  for (auto& g : ctx->graphs) {
+    cudaGraphExecDestroy(g.exec);
+    for (auto& mk : g.marks) {
+      cudaEventDestroy(mk.a);
+      cudaEventDestroy(mk.b);
+    }
+  }
+  ctx->graphs.clear();
 }
 
 inline unsigned blocks_for(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
@@ -376,8 +415,10 @@ int rebin(mpm_ctx* ctx) {
       ctx->bperm, ctx->n, ctx->cap);
   LAUNCHED();
   ctx->cur = nxt;
+  // ~4 items per SM at least: small scenes split bins, large ones keep whole bins
+  const int chunk = (int)std::max<long long>(MIN_CHUNK, std::min<long long>(CHUNK, ctx->n / (4LL * ctx->sms)));
   make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(
-      ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, ctx->counters + 1);
+      ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, ctx->counters + 1, chunk);
   LAUNCHED();
   return 0;
 }
@@ -488,6 +529,24 @@ int read_inverted(mpm_ctx* ctx, int64_t* out) {
   return 0;
 }
 
+// The fast-path frame: re-binning + L-substep stretches (captured as a graph).
+int run_fast_sequence(mpm_ctx* ctx, int nsub, bool col) {
+  TRY(ensure_gm_clean(ctx));
+  int s = 0;
+  while (s < nsub) {
+    const int L = std::min(ctx->cfg.rebin_interval, nsub - s);
+    TRY(rebin(ctx));
+    for (int t = 0; t < L; ++t) {
+      TRY(launch_fused(ctx, t > 0));
+      TRY(launch_grid_op(ctx, false, col, s + t, s + t != nsub - 1));
+    }
+    TRY(launch_g2p(ctx));
+    s += L;
+  }
+  ctx->grid_dirty = 1;
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -539,6 +598,8 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     {
       const char* e = getenv("SOFTMPM_SPLIT");
       ctx->split_mode = e && e[0] == '1';
+      const char* g = getenv("SOFTMPM_GRAPHS");
+      ctx->graphs_on = !(g && g[0] == '0');
     }
     cudaFuncSetAttribute(g2p_stress_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(float) * 6 * TILE_NODES));
@@ -570,6 +631,7 @@ int mpm_destroy(mpm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  invalidate_graphs(ctx);
   void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box,
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
@@ -592,6 +654,7 @@ int mpm_destroy(mpm_ctx* ctx) {
 
 int mpm_set_config(mpm_ctx* ctx, const mpm_config* cfg) {
   if (!ctx || !cfg) return MPM_EINVAL;
+  invalidate_graphs(ctx);
   std::string why;
   if (validate(cfg, why)) return fail(ctx, MPM_EINVAL, why);
   for (int a = 0; a < 3; ++a)
@@ -607,6 +670,7 @@ int mpm_set_config(mpm_ctx* ctx, const mpm_config* cfg) {
 int mpm_set_materials(mpm_ctx* ctx, const double* mu, const double* lam, int count) {
   if (!ctx || !mu || !lam || count <= 0) return fail(ctx, MPM_EINVAL, "materials: bad arguments");
   CK(cudaSetDevice(ctx->dev));
+  if (count != ctx->nmat) invalidate_graphs(ctx);
   std::vector<float> m(count), l(count);
   for (int i = 0; i < count; ++i) {
     m[i] = (float)mu[i];
@@ -632,6 +696,7 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
     if (material_id[i] < 0 || (ctx->nmat > 0 && material_id[i] >= ctx->nmat))
       return fail(ctx, MPM_EINVAL, "material id out of range");
   CK(cudaSetDevice(ctx->dev));
+  invalidate_graphs(ctx);
   if (n > ctx->cap) {
     long long cap = n;
     for (int b = 0; b < 2; ++b) {
@@ -645,10 +710,11 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
     TRY(dalloc(ctx, &ctx->sidx, (size_t)cap));
     TRY(dalloc(ctx, &ctx->slc, (size_t)cap));
     TRY(dalloc(ctx, &ctx->bperm, (size_t)cap));
-    ctx->work_cap = ctx->nbins + cap / CHUNK + 1;
+    ctx->work_cap = ctx->nbins + cap / MIN_CHUNK + 1;
     TRY(dalloc(ctx, &ctx->work, (size_t)ctx->work_cap));
     TRY(dalloc(ctx, &ctx->item_bounds, (size_t)ctx->work_cap));
     TRY(dalloc(ctx, &ctx->item_bounds2, (size_t)ctx->work_cap));
+    ctx->bounds_a = ctx->item_bounds;
     TRY(dalloc(ctx, &ctx->pay, (size_t)cap * NPAY));
     TRY(dalloc(ctx, &ctx->item_box, (size_t)ctx->work_cap));
     if (ctx->perm) {
@@ -768,6 +834,7 @@ int mpm_set_colliders(mpm_ctx* ctx, int count, const int32_t* kind, const double
                       const double* sdf_extent) {
   if (!ctx || count < 0 || count > MAX_COLLIDERS) return fail(ctx, MPM_EINVAL, "set_colliders: bad count");
   CK(cudaSetDevice(ctx->dev));
+  invalidate_graphs(ctx);
   ctx->ncol = count;
   ctx->geo_h.assign(std::max(count, 1), ColliderGeo{});
   std::vector<ColliderPose> pose(std::max(count, 1));
@@ -849,6 +916,7 @@ int mpm_set_pose_table(mpm_ctx* ctx, int nsub, const double* rotation, const dou
       q.mode = mode ? mode[r] : ctx->geo_h[i].mode;
     }
   if (ctx->pose_cap < nsub) {
+    invalidate_graphs(ctx);
     TRY(dalloc(ctx, &ctx->pose, (size_t)nsub * MAX_COLLIDERS));
     ctx->pose_cap = nsub;
   }
@@ -910,20 +978,68 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       TRY(launch_g2p(ctx));
     }
     ctx->grid_dirty = 2;
+  } else if (!ctx->graphs_on) {
+    TRY(run_fast_sequence(ctx, nsub, col));
   } else {
-    TRY(ensure_gm_clean(ctx));
-    int s = 0;
-    while (s < nsub) {
-      int L = std::min(ctx->cfg.rebin_interval, nsub - s);
-      TRY(rebin(ctx));
-      for (int t = 0; t < L; ++t) {
-        TRY(launch_fused(ctx, t > 0));
-        TRY(launch_grid_op(ctx, false, col, s + t, s + t != nsub - 1));
+    const int border = ctx->item_bounds == ctx->bounds_a ? 0 : 1;
+    const int timing = ctx->timing ? 1 : 0;
+    mpm_ctx::GraphEntry* hit = nullptr;
+    for (auto& g : ctx->graphs)
+      if (g.nsub == nsub && g.col == (int)col && g.cur == ctx->cur && g.border == border &&
+          g.dirty == ctx->grid_dirty && g.timing == timing && g.n == ctx->n)
+        hit = &g;
+    if (!hit) {
+      mpm_ctx::GraphEntry e{};
+      e.nsub = nsub;
+      e.col = (int)col;
+      e.cur = ctx->cur;
+      e.border = border;
+      e.dirty = ctx->grid_dirty;
+      e.timing = timing;
+      e.n = ctx->n;
+      const size_t marks0 = ctx->marks.size();
+      const long long launches0 = ctx->launches;
+      CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      const int rc = run_fast_sequence(ctx, nsub, col);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+      if (rc || ce != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        if (!rc) ctx->err = std::string("graph capture: ") + cudaGetErrorString(ce);
+        return rc ? rc : MPM_ECUDA;
       }
-      TRY(launch_g2p(ctx));
-      s += L;
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        ctx->err = std::string("graph instantiate: ") + cudaGetErrorString(ie);
+        return MPM_ECUDA;
+      }
+      for (size_t i = marks0; i < ctx->marks.size(); ++i) {
+        e.marks.push_back(ctx->marks[i]);
+        e.marks.back().graph_owned = true;
+      }
+      ctx->marks.resize(marks0);
+      e.kernels = ctx->launches - launches0;
+      ctx->launches = launches0;
+      e.end_cur = ctx->cur;
+      e.end_border = ctx->item_bounds == ctx->bounds_a ? 0 : 1;
+      e.end_dirty = ctx->grid_dirty;
+      // the capture advanced the host state as a real run would; restore the
+      // start state so the replay below applies the same transition
+      ctx->cur = e.cur;
+      if ((ctx->item_bounds == ctx->bounds_a ? 0 : 1) != e.border) std::swap(ctx->item_bounds, ctx->item_bounds2);
+      ctx->grid_dirty = e.dirty;
+      ctx->graphs.push_back(std::move(e));
+      hit = &ctx->graphs.back();
     }
-    ctx->grid_dirty = 1;
+    CK(cudaGraphLaunch(hit->exec, ctx->stream));
+    ctx->launches += hit->kernels;
+    ctx->cur = hit->end_cur;
+    if ((ctx->item_bounds == ctx->bounds_a ? 0 : 1) != hit->end_border) std::swap(ctx->item_bounds, ctx->item_bounds2);
+    ctx->grid_dirty = hit->end_dirty;
+    if (timing)
+      for (auto& mk : hit->marks) ctx->marks.push_back(mk);
   }
   ctx->grid_phase = 1;
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
@@ -932,6 +1048,21 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     *device_ms = ms;
+  }
+  return 0;
+}
+
+int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
+  if (!ctx || !key) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  if (!strcmp(key, "graphs")) {
+    invalidate_graphs(ctx);
+    ctx->graphs_on = value != 0;
+  } else if (!strcmp(key, "split")) {
+    invalidate_graphs(ctx);
+    ctx->split_mode = value != 0;
+  } else {
+    return fail(ctx, MPM_EINVAL, std::string("unknown option ") + key);
   }
   return 0;
 }
