@@ -124,6 +124,10 @@ class ClockSampler:
 
 def build_scene(config: str, particles: int | None, seed: int):
     from paper_2402_01181_b200 import scenes
+    if config == "c4":  # CPU legs: one environment (environments run sequentially on the CPU)
+        b, mats, params, fns = scenes.c4_envs(count=particles or 30_000, env_ids=[seed - 1])
+        st = b.state
+        return st, mats, params, [c for c in b.colliders[0]], fns[0]
     kw = {"seed": seed}
     if particles:
         kw["count"] = particles
@@ -220,27 +224,74 @@ def run_ours(args, rank, world, local_rank):
     dist = world > 1
     if dist:
         import torch.distributed as tdist
-    st, mats, params, cols, pose_fn = build_scene(args.config, args.particles, 1 + rank)
-    st.device = local_rank
+    if args.config == "c4":
+        from paper_2402_01181_b200 import scenes
+        from paper_2402_01181_b200.batch import shard
+        env_ids = list(shard(args.envs, world, rank))
+        batch, mats, params, _ = scenes.c4_envs(count=args.particles or 30_000, env_ids=env_ids)
+        st = batch.state
+        st.device = local_rank
+        cols = batch._proxies
+        nsub = params.substeps_per_frame
+        traj = scenes.c4_trajectory()
+
+        def c4_poses(t0):
+            E = batch.n_envs
+            R = np.broadcast_to(np.eye(3), (nsub, E, 1, 3, 3)).copy()
+            T = np.zeros((nsub, E, 1, 3))
+            lv = np.zeros((nsub, E, 1, 3))
+            t = t0
+            for s in range(nsub):  # every environment follows the same tool path
+                poses, _ = sm.pose_at(traj, t)
+                T[s, :, 0] = poses[0][0]
+                lv[s, :, 0] = poses[0][2]
+                t += params.dt
+            return {"R": R, "T": T, "lv": lv}
+
+        def rows_for(t0):
+            return batch.pose_rows(c4_poses(t0))
+
+        def warm():
+            batch.step(mats, params, poses=c4_poses(batch.time))
+
+        workload = (f"c4: {batch.n_envs} environments/GPU x {args.particles or 30_000} particles "
+                    f"(64^3 each, tiles {batch.tiles}), box tool each, 25 substeps per step")
+    else:
+        st, mats, params, cols, pose_fn = build_scene(args.config, args.particles, 1 + rank)
+        st.device = local_rank
+        batch = None
+
+        def rows_for(t0):
+            return pose_rows(st, cols, params, pose_fn, t0)
+
+        def warm():
+            sm.step(st, mats, params, cols, pose_fn)
+
+        workload = (f"{args.config}: {st.particle_count} particles/GPU, {st.grid.resolution[0]}^3 grid, "
+                    f"{len(cols)} tool(s)" + (" pressing 3 cm at 0.5 m/s then holding" if args.config == "c3" else "")
+                    + ", 25 substeps per step")
     n = st.particle_count
     nsub = params.substeps_per_frame
     L = _lib.lib()
 
-    # warm-up through the public API (creates the context, uploads, JITs nothing)
+    # warm-up through the public API (creates the context, uploads, captures graphs)
     for _ in range(args.warmup):
-        sm.step(st, mats, params, cols, pose_fn)
+        warm()
     ctx = st._ctx
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
 
     def frame():
-        rows = pose_rows(st, cols, params, pose_fn, st.time) if cols else None
+        t0 = batch.time if batch is not None else st.time
         if cols:
-            st._upload_pose_rows(*rows)
+            st._upload_pose_rows(*rows_for(t0))
         inv = ctypes.c_int64(0)
         ms = ctypes.c_double(0.0)
         ctx.call("mpm_substeps", nsub, int(bool(cols)), ctypes.byref(inv), ctypes.byref(ms))
         for _ in range(nsub):
-            st.time += params.dt
+            if batch is not None:
+                batch.time += params.dt
+            else:
+                st.time += params.dt
         st._device_wrote(("x", "v", "F", "C"))
         return ms.value
 
@@ -329,9 +380,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": 1000.0 * t_dev / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {n} particles/GPU, {st.grid.resolution[0]}^3 grid, "
-                   f"{len(cols)} box tool(s) pressing 3 cm at 0.5 m/s then holding, 25 substeps per step",
-                   "particles_per_gpu": n, "grid": list(st.grid.resolution),
+        "config": {"workload": workload, "particles_per_gpu": n, "grid": list(st.grid.resolution),
                    "substeps_per_step": nsub, "parallelism": f"replicas x{world}",
                    "l2": "flushed between steps (512 MiB memset)",
                    "wall_s_timed": wall},
@@ -369,7 +418,8 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--envs", type=int, default=1024, help="c4: environments over all ranks")
     ap.add_argument("--particles", type=int, default=None)
     ap.add_argument("--cpu-substeps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -59,6 +59,13 @@ typedef struct {
   int mode_live;        /* 0: collider mode frozen at first pack (F7 compat), 1: live */
   int deterministic;    /* 1: sorted deterministic-order P2G (bit-exact grid mass) */
   int rebin_interval;   /* substeps between particle re-binning (fast mode), >= 1 */
+  /* Batched independent environments (BASELINE config 4): the grid is
+   * env_tiles[0] x env_tiles[1] x env_tiles[2] tiles of res/env_tiles nodes,
+   * one environment per tile with its own domain walls and margins; the
+   * collider table holds colliders_per_env colliders per tile, tile-major.
+   * {0,0,0} or {1,1,1}: one environment. */
+  int env_tiles[3];
+  int colliders_per_env; /* 0: every collider acts on the whole grid */
 } mpm_config;
 
 /* ---- lifetime ---------------------------------------------------------- */

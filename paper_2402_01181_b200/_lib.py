@@ -44,7 +44,8 @@ class MpmConfig(ctypes.Structure):
                 ("boundary_width", ctypes.c_int), ("stick", ctypes.c_int),
                 ("theta", ctypes.c_double), ("stress_form", ctypes.c_int),
                 ("mode_live", ctypes.c_int), ("deterministic", ctypes.c_int),
-                ("rebin_interval", ctypes.c_int)]
+                ("rebin_interval", ctypes.c_int), ("env_tiles", ctypes.c_int * 3),
+                ("colliders_per_env", ctypes.c_int)]
 
 
 def build(force: bool = False) -> str:

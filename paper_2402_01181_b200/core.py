@@ -161,6 +161,8 @@ class SimState:
         self._packed_for: tuple[int, ...] = ()
         self._collision_cache: CollisionField | None = None
         self._collision_src = None
+        self._env_tiles = (1, 1, 1)   # set by batch.EnvBatch (BASELINE config 4)
+        self._colliders_per_env = 0
 
     # ---------------------------------------------------------------- fields
     def _get(self, name: str) -> np.ndarray:
@@ -290,6 +292,8 @@ class SimState:
         cfg.mode_live = int(params.collider_mode == "live")
         cfg.deterministic = int(bool(params.deterministic))
         cfg.rebin_interval = int(params.rebin_interval)
+        cfg.env_tiles = (ctypes.c_int * 3)(*self._env_tiles)
+        cfg.colliders_per_env = int(self._colliders_per_env)
         return cfg
 
     def _prepare(self, materials, params: SimParams, theta: float | None = None) -> _lib.Context:

@@ -43,13 +43,25 @@ struct ColliderPose {
 };
 
 struct Colliders {
-  int count;
-  double theta;  // < 0: disabled
+  int count;      // colliders acting on one environment tile
+  double theta;   // < 0: disabled
   float theta_f;  // theta + prefilter margin (fp32)
   const ColliderGeo* geo;
   const ColliderPose* pose;  // row for this substep
   const double* sdf;
+  int per_env;        // 0: one table for the whole grid; else count per tile, tile-major
+  int env_tiles[3];
 };
+
+// The collider sub-table of environment tile (ei, ej, ek).
+__device__ __forceinline__ Colliders env_colliders(const Colliders& cs, int ei, int ej, int ek) {
+  if (!cs.per_env) return cs;
+  Colliders c = cs;
+  const int e = (ei * cs.env_tiles[1] + ej) * cs.env_tiles[2] + ek;
+  c.geo += (long long)e * cs.per_env;
+  c.pose += (long long)e * cs.per_env;
+  return c;
+}
 
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }

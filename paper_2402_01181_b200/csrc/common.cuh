@@ -44,7 +44,9 @@ struct Params {
   int nbin[3];     // particle bins per axis
   float dx, inv_dx, dt;
   float gravity[3];
-  float lo, hi[3];  // particle margin clamp (core.py:51-56)
+  float lo, hi[3];  // particle margin clamp (core.py:51-56), env-local
+  int env_res[3];   // nodes per environment tile (== res for one environment)
+  float env_ext[3]; // env_res * dx
   float stress_coef;  // -4 dt / dx^2 (kernels.py:207)
   float apic_coef;    // 4 / dx^2 (kernels.py:448)
   double dx64, dt64;

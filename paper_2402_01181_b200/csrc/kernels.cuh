@@ -147,12 +147,15 @@ __device__ __forceinline__ void g2p_gather(const Params& p, const float x[3], fl
   g2p_gather(p, global_vel(p), b, f, w, v, C);
 }
 
+// x += dt v, clamped to the margins of the particle's environment tile
+// (core.py:51-56, kernels.py:517-534; one tile = the whole grid normally).
 __device__ __forceinline__ void advect(const Params& p, float x[3], const float v[3]) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
+    const float org = p.env_res[a] == p.res[a] ? 0.0f : floorf(x[a] / p.env_ext[a]) * p.env_ext[a];
     float q = x[a] + p.dt * v[a];
-    q = q < p.lo ? p.lo : q;
-    q = q > p.hi[a] ? p.hi[a] : q;
+    q = q < org + p.lo ? org + p.lo : q;
+    q = q > org + p.hi[a] ? org + p.hi[a] : q;
     x[a] = q;
   }
 }
@@ -881,9 +884,13 @@ __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
 // (collide.cuh: collider_far) is below theta + margin -- nodes the bound
 // clears cannot be in contact, so results are unchanged.  When `clear`, gm
 // is zeroed for the next P2G.
-__device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs, double cap, float4 a, int gi,
+__device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs_all, double cap, float4 a, int gi,
                                             int gj, int gk) {
   if (!(a.w > 0.0f) || gi >= p.res[0] || gj >= p.res[1] || gk >= p.res[2]) return a;
+  // environment tile of this node: local coordinates + its colliders
+  const int ei = gi / p.env_res[0], ej = gj / p.env_res[1], ek = gk / p.env_res[2];
+  const Colliders cs = env_colliders(cs_all, ei, ej, ek);
+  const int li = gi - ei * p.env_res[0], lj = gj - ej * p.env_res[1], lk = gk - ek * p.env_res[2];
   const float inv_m = 1.0f / a.w;
   float v0 = a.x * inv_m + p.dt * p.gravity[0];
   float v1 = a.y * inv_m + p.dt * p.gravity[1];
@@ -906,16 +913,16 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
     }
   }
   const int bw = p.bwidth;
+  const int rx = p.env_res[0], ry = p.env_res[1], rz = p.env_res[2];
   if (p.stick) {
-    if (gi < bw || gi >= p.res[0] - bw || gj < bw || gj >= p.res[1] - bw || gk < bw || gk >= p.res[2] - bw)
-      v0 = v1 = v2 = 0.0f;
+    if (li < bw || li >= rx - bw || lj < bw || lj >= ry - bw || lk < bw || lk >= rz - bw) v0 = v1 = v2 = 0.0f;
   } else {
-    if (gi < bw && v0 < 0.0f) v0 = 0.0f;
-    if (gi >= p.res[0] - bw && v0 > 0.0f) v0 = 0.0f;
-    if (gj < bw && v1 < 0.0f) v1 = 0.0f;
-    if (gj >= p.res[1] - bw && v1 > 0.0f) v1 = 0.0f;
-    if (gk < bw && v2 < 0.0f) v2 = 0.0f;
-    if (gk >= p.res[2] - bw && v2 > 0.0f) v2 = 0.0f;
+    if (li < bw && v0 < 0.0f) v0 = 0.0f;
+    if (li >= rx - bw && v0 > 0.0f) v0 = 0.0f;
+    if (lj < bw && v1 < 0.0f) v1 = 0.0f;
+    if (lj >= ry - bw && v1 > 0.0f) v1 = 0.0f;
+    if (lk < bw && v2 < 0.0f) v2 = 0.0f;
+    if (lk >= rz - bw && v2 > 0.0f) v2 = 0.0f;
   }
   return make_float4(v0, v1, v2, a.w);
 }
@@ -1338,8 +1345,9 @@ __global__ void collision_field_kernel(Params p, Colliders cs, double cap, doubl
   int gk = (int)(node % p.res[2]);
   int gj = (int)((node / p.res[2]) % p.res[1]);
   int gi = (int)(node / ((long long)p.res[1] * p.res[2]));
+  const Colliders ce = env_colliders(cs, gi / p.env_res[0], gj / p.env_res[1], gk / p.env_res[2]);
   double best;
-  int id = nearest_collider(cs, (double)gi * p.dx64, (double)gj * p.dx64, (double)gk * p.dx64, cap, best);
+  int id = nearest_collider(ce, (double)gi * p.dx64, (double)gj * p.dx64, (double)gk * p.dx64, cap, best);
   dist[node] = best;
   obj[node] = id;
 }

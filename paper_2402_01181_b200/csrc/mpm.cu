@@ -76,7 +76,7 @@ struct mpm_ctx {
   int ncol = 0;
   ColliderGeo* geo = nullptr;
   ColliderPose* pose = nullptr;
-  int pose_rows = 0, pose_cap = 0;
+  int pose_rows = 0, pose_cap = 0, pose_width = 0;
   double* sdf = nullptr;
   std::vector<ColliderGeo> geo_h;
 
@@ -245,7 +245,10 @@ Params make_params(mpm_ctx* ctx) {
     p.nb[a] = (c.res[a] + 3) / 4;
     p.nbin[a] = ctx->nbin[a];
     p.gravity[a] = (float)c.gravity[a];
-    double hd = (c.res[a] - 1.5 - 1.0e-7) * c.dx;
+    const int et = c.env_tiles[a] > 1 ? c.env_tiles[a] : 1;
+    p.env_res[a] = c.res[a] / et;
+    p.env_ext[a] = (float)(p.env_res[a] * c.dx);
+    double hd = (p.env_res[a] - 1.5 - 1.0e-7) * c.dx;
     float hf = (float)hd;
     if ((double)hf > hd) hf = std::nextafter(hf, 0.0f);
     p.hi[a] = hf;
@@ -281,7 +284,10 @@ Params make_params(mpm_ctx* ctx) {
 
 Colliders make_colliders(mpm_ctx* ctx, int row, bool use) {
   Colliders cs{};
-  cs.count = use ? ctx->ncol : 0;
+  const int per_env = ctx->cfg.colliders_per_env > 0 ? ctx->cfg.colliders_per_env : 0;
+  cs.count = use ? (per_env ? per_env : ctx->ncol) : 0;
+  cs.per_env = per_env;
+  for (int a = 0; a < 3; ++a) cs.env_tiles[a] = ctx->cfg.env_tiles[a] > 1 ? ctx->cfg.env_tiles[a] : 1;
   cs.theta = use && ctx->ncol > 0 ? ctx->cfg.theta : -1.0;
   cs.geo = ctx->geo;
   int r = ctx->pose_rows > 0 ? std::min(row, ctx->pose_rows - 1) : 0;
@@ -302,6 +308,11 @@ int validate(const mpm_config* c, std::string& why) {
   if (!(c->dt > 0.0)) { why = "dt must be positive"; return 1; }
   if (c->boundary_width < 0) { why = "boundary_width must be >= 0"; return 1; }
   if (c->stress_form != 0 && c->stress_form != 1) { why = "unknown stress form"; return 1; }
+  for (int a = 0; a < 3; ++a) {
+    const int et = c->env_tiles[a] > 1 ? c->env_tiles[a] : 1;
+    if (c->res[a] % et != 0 || c->res[a] / et < 8) { why = "env_tiles must divide res into tiles of >= 8 nodes"; return 1; }
+  }
+  if (c->colliders_per_env < 0) { why = "colliders_per_env must be >= 0"; return 1; }
   double nodes = (double)((c->res[0] + 3) / 4) * ((c->res[1] + 3) / 4) * ((c->res[2] + 3) / 4) * 64.0;
   if (nodes >= 2147483647.0) { why = "grid too large for 32-bit node indexing on one device"; return 1; }
   return 0;
@@ -832,7 +843,16 @@ int mpm_set_colliders(mpm_ctx* ctx, int count, const int32_t* kind, const double
                       const double* friction, const int32_t* mode, const double* sdf_values, int64_t sdf_len,
                       const int64_t* sdf_offset, const int32_t* sdf_resolution, const double* sdf_bounds_min,
                       const double* sdf_extent) {
-  if (!ctx || count < 0 || count > MAX_COLLIDERS) return fail(ctx, MPM_EINVAL, "set_colliders: bad count");
+  if (!ctx || count < 0) return fail(ctx, MPM_EINVAL, "set_colliders: bad count");
+  {
+    const int per = ctx->cfg.colliders_per_env > 0 ? ctx->cfg.colliders_per_env : count;
+    if (per > MAX_COLLIDERS) return fail(ctx, MPM_EINVAL, "set_colliders: too many colliders per environment");
+    if (ctx->cfg.colliders_per_env > 0) {
+      int tiles = 1;
+      for (int a = 0; a < 3; ++a) tiles *= ctx->cfg.env_tiles[a] > 1 ? ctx->cfg.env_tiles[a] : 1;
+      if (count != per * tiles) return fail(ctx, MPM_EINVAL, "set_colliders: count != colliders_per_env x env tiles");
+    }
+  }
   CK(cudaSetDevice(ctx->dev));
   invalidate_graphs(ctx);
   ctx->ncol = count;
@@ -880,9 +900,10 @@ int mpm_set_colliders(mpm_ctx* ctx, int count, const int32_t* kind, const double
   TRY(dalloc(ctx, &ctx->geo, (size_t)std::max(count, 1)));
   CK(cudaMemcpyAsync(ctx->geo, ctx->geo_h.data(), sizeof(ColliderGeo) * std::max(count, 1), cudaMemcpyHostToDevice,
                      ctx->stream));
-  if (ctx->pose_cap < 1) {
-    TRY(dalloc(ctx, &ctx->pose, (size_t)MAX_COLLIDERS));
+  if (ctx->pose_cap < 1 || ctx->pose_width < std::max(count, 1)) {
+    TRY(dalloc(ctx, &ctx->pose, (size_t)std::max(count, MAX_COLLIDERS)));
     ctx->pose_cap = 1;
+    ctx->pose_width = std::max(count, MAX_COLLIDERS);
   }
   CK(cudaMemcpyAsync(ctx->pose, pose.data(), sizeof(ColliderPose) * std::max(count, 1), cudaMemcpyHostToDevice,
                      ctx->stream));
@@ -915,10 +936,12 @@ int mpm_set_pose_table(mpm_ctx* ctx, int nsub, const double* rotation, const dou
       }
       q.mode = mode ? mode[r] : ctx->geo_h[i].mode;
     }
-  if (ctx->pose_cap < nsub) {
+  if (ctx->pose_cap < nsub || ctx->pose_width < k) {
     invalidate_graphs(ctx);
-    TRY(dalloc(ctx, &ctx->pose, (size_t)nsub * MAX_COLLIDERS));
+    const int width = std::max(k, MAX_COLLIDERS);
+    TRY(dalloc(ctx, &ctx->pose, (size_t)nsub * width));
     ctx->pose_cap = nsub;
+    ctx->pose_width = width;
   }
   CK(cudaMemcpyAsync(ctx->pose, rows.data(), sizeof(ColliderPose) * rows.size(), cudaMemcpyHostToDevice, ctx->stream));
   ctx->pose_rows = nsub;

@@ -78,4 +78,35 @@ def c3(count: int = 1_000_000, res: int = 256, seed: int = 1):
     return st, mats, SimParams(), cols, pose_fn
 
 
+def c4_trajectory():
+    """Tool path of every config-4 environment: press 2.5 cm at 0.5 m/s, hold."""
+    y0 = 0.23 + 0.035 + 0.005
+    return [Keyframe(0.0, [(np.array([0.5, y0, 0.5]), _Q)]),
+            Keyframe(0.05, [(np.array([0.5, y0 - 0.025, 0.5]), _Q)]),
+            Keyframe(10.0, [(np.array([0.5, y0 - 0.025, 0.5]), _Q)])]
+
+
+def c4_envs(n_envs: int = 1024, count: int = 30_000, res: int = 64, first_seed: int = 1,
+            env_ids=None):
+    """Config 4: independent config-1-style environments (seed = env index),
+    each with a box tool pressing 2 cm into its block at 0.5 m/s then holding;
+    returns an EnvBatch plus (materials, params, pose_fns)."""
+    from .batch import EnvBatch
+
+    ids = list(env_ids) if env_ids is not None else list(range(n_envs))
+    grid = Grid((res, res, res))
+    mats = _material()
+    states, cols, fns = [], [], []
+    for e in ids:
+        spawn = sample_box((0.5, 0.13, 0.5), (0.3, 0.2, 0.3), count, seed=first_seed + e, grid=grid)
+        states.append(SimState.from_spawns(grid, [spawn], mats))
+        traj = c4_trajectory()
+        c = [RigidCollider(id=0, shape=Box(np.array([0.06, 0.035, 0.06])), friction_mu=0.4)]
+        fn = make_pose_fn(traj)
+        fn(c, 0.0)
+        cols.append(c)
+        fns.append(fn)
+    return EnvBatch(states, cols), mats, SimParams(), fns
+
+
 BUILDERS = {"c1": c1, "c2": c2, "c3": c3}

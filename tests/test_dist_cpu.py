@@ -1,0 +1,60 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): environment sharding and
+the max-over-ranks throughput reduction used by bench.py."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2402_01181_b200.batch import shard, tile_shape
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n_envs, out):
+    import torch.distributed as dist
+    from paper_2402_01181_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, r, lr = D.world()
+        assert (w, r, lr) == (world, rank, rank)
+        mine = shard(n_envs, w, r)
+        units = len(mine) * 1000.0          # particle-substeps done by this rank
+        seconds = 1.0 + rank                # rank 1 is the slow one
+        tp = D.throughput(units, seconds)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, list(mine))
+        out[rank] = (tp, gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_envs", [1024, 7])
+def test_gloo_two_ranks_shard_and_throughput(n_envs):
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), n_envs, out), nprocs=world, join=True)
+    tp0, envs = out[0]
+    assert out[1][0] == tp0
+    assert tp0 == pytest.approx(n_envs * 1000.0 / 2.0)  # total units / max time
+    flat = [e for part in envs for e in part]
+    assert flat == list(range(n_envs))                  # every env exactly once, contiguous
+
+
+def test_shard_and_tiles_single_process():
+    for n in (1, 5, 1024):
+        for w in (1, 2, 3, 8):
+            parts = [shard(n, w, r) for r in range(w)]
+            assert sum(len(p) for p in parts) == n
+            assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+    for n in (1, 3, 8, 100, 1024):
+        t = tile_shape(n)
+        assert t[0] * t[1] * t[2] >= n
+        assert t[0] * t[1] * t[2] < 2 * n + 2

@@ -152,3 +152,59 @@ def test_install_reroutes_reference_shaped_module():
         sm.uninstall(ref)
     with pytest.raises(AssertionError):
         ref.step(st, mats, sm.SimParams())
+
+
+def test_env_batch_matches_isolated_runs_and_oracle():
+    """Config 4: environments packed as tiles of one context behave like
+    isolated runs (and like the CPU oracle), with per-tile walls and tools."""
+    ids = [0, 1, 2, 3, 4]
+    batch, mats, params, fns = scenes.c4_envs(n_envs=5, count=4000, res=64, env_ids=ids)
+    assert batch.tiles == (1, 1, 5) or int(np.prod(batch.tiles)) >= 5
+    singles = [scenes.c4_envs(count=4000, res=64, env_ids=[e]) for e in ids]
+    ref_b, _, _, ref_fns = scenes.c4_envs(count=4000, res=64, env_ids=[2])
+    osim = _oracle_for(ref_b.state, mats)
+    ocols = [sm.RigidCollider(id=0, shape=sm.Box(np.array([0.06, 0.035, 0.06])), friction_mu=0.4)]
+    t = 0.0
+    for _ in range(4):
+        batch.step(mats, params, fns)
+        for b1, _, _, f1 in singles:
+            b1.step(mats, params, f1)
+        for _ in range(params.substeps_per_frame):
+            ref_fns[0](ocols, t)
+            osim.substep(sm.pack_colliders(ocols))
+            t += params.dt
+    for e, (b1, _, _, _) in zip(ids, singles):
+        for k in ("x", "v", "F"):
+            assert rel_l2(batch.field(k, e), b1.field(k, 0)) < 1e-4, (e, k)
+    for k in ("x", "v", "F"):
+        assert rel_l2(batch.field(k, 2), getattr(osim, k)) < 1e-3, k
+    # tools act: the pressed top layer moved down in every environment
+    for e in ids:
+        assert batch.field("v", e)[:, 1].min() < -0.05
+
+
+def test_env_batch_vectorised_pose_table():
+    batch, mats, params, fns = scenes.c4_envs(n_envs=3, count=3000, res=64)
+    ref, _, _, rfns = scenes.c4_envs(n_envs=3, count=3000, res=64)
+    nsub = params.substeps_per_frame
+    t = np.arange(nsub) * params.dt
+    R = np.broadcast_to(np.eye(3), (nsub, 3, 1, 3, 3)).copy()
+    T = np.zeros((nsub, 3, 1, 3))
+    lv = np.zeros((nsub, 3, 1, 3))
+    for s in range(nsub):
+        for e in range(3):
+            poses, _ = sm.pose_at(_traj_c4(), t[s])
+            T[s, e, 0] = poses[0][0]
+            lv[s, e, 0] = poses[0][2]
+    batch.step(mats, params, poses={"R": R, "T": T, "lv": lv})
+    ref.step(mats, params, rfns)
+    for e in range(3):
+        assert rel_l2(batch.field("x", e), ref.field("x", e)) < 1e-6
+
+
+def _traj_c4():
+    q = np.array([0.0, 0.0, 0.0, 1.0])
+    y0 = 0.23 + 0.035 + 0.005
+    return [sm.Keyframe(0.0, [(np.array([0.5, y0, 0.5]), q)]),
+            sm.Keyframe(0.05, [(np.array([0.5, y0 - 0.025, 0.5]), q)]),
+            sm.Keyframe(10.0, [(np.array([0.5, y0 - 0.025, 0.5]), q)])]
