@@ -224,6 +224,8 @@ def run_ours(args, rank, world, local_rank):
     dist = world > 1
     if dist:
         import torch.distributed as tdist
+    if args.config == "c5" and world > 1:
+        return run_slab(args, rank, world, local_rank)
     if args.config == "c4":
         from paper_2402_01181_b200 import scenes
         from paper_2402_01181_b200.batch import shard
@@ -401,7 +403,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.config != "c5":
         threads = os.cpu_count() or 1
         rate, times, nn = cpu_oracle_rate(args.config, args.particles, 1, args.cpu_substeps, threads)
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
@@ -412,13 +414,57 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(out), flush=True)
 
 
+def run_slab(args, rank, world, local_rank):
+    """Config 5 across ranks: x-slab windows, NCCL halo exchange + migration."""
+    import torch
+    import torch.distributed as tdist
+    import paper_2402_01181_b200 as sm
+    from paper_2402_01181_b200 import scenes, slab
+    from paper_2402_01181_b200.dist import max_over_ranks, sum_over_ranks
+    st, mats, params, _, _ = scenes.c5(count=args.particles or 64_000_000)
+    g = st.grid
+    x, v, F, C = st.x, st.v, st.F, st.C
+    wins = slab.split_state(g, x, v, F, C, st.mass, st.vol0, st.material_id, ranks=world,
+                            ghost_bricks=2, device=local_rank)
+    win = wins[rank]
+    del wins, st, x, v, F, C
+    ex = slab.TorchExchange(win, rank, world, device=f"cuda:{local_rank}")
+    for _ in range(args.warmup):
+        slab.step_distributed(win, ex, mats, params)
+    n_local = int(_lib_count(win))
+    tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        slab.step_distributed(win, ex, mats, params)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    el = max_over_ranks(time.perf_counter() - t0, f"cuda:{local_rank}")
+    n_total = sum_over_ranks(n_local, f"cuda:{local_rank}")
+    if rank == 0:
+        value = n_total * params.substeps_per_frame * args.steps / el
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"c5: {int(n_total)} particles, {g.resolution[0]}^3 grid, x-slabs over "
+                                   f"{world} GPUs (NCCL halo + migration; wall clock incl. exchanges)",
+                       "parallelism": f"slab x{world}"},
+        }), flush=True)
+
+
+def _lib_count(win):
+    from paper_2402_01181_b200 import _lib
+    return _lib.lib().mpm_particle_count(win.state._ctx.h)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--envs", type=int, default=1024, help="c4: environments over all ranks")
     ap.add_argument("--particles", type=int, default=None)
     ap.add_argument("--cpu-substeps", type=int, default=3)

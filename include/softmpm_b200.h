@@ -128,6 +128,40 @@ int mpm_g2p(mpm_ctx *ctx);
 int mpm_substeps(mpm_ctx *ctx, int nsub, int use_colliders, int64_t *inverted,
                  double *device_ms);
 
+/* ---- slab decomposition (BASELINE config 5) ------------------------------
+ * A context can own an x-window of a larger global grid: its res[0] nodes
+ * start at global node offset[0] (multiple of 4) and include `ghost_bricks`
+ * 4-node brick layers on each side owned by the neighbouring windows.  Walls,
+ * colliders and margins use global coordinates; device particle positions
+ * are window-local.  Per substep the driver calls
+ *   mpm_stage_particles -> mpm_halo_pack (both sides) -> exchange ->
+ *   mpm_halo_unpack_add -> mpm_stage_grid -> mpm_halo_pack_vel -> exchange ->
+ *   mpm_halo_unpack_vel
+ * (exchange = NCCL send/recv of the buffers of mpm_halo_buffers, or device
+ * copies between contexts of one process), and at stretch boundaries
+ * mpm_stage_end -> mpm_extract_migrants -> exchange -> mpm_append_particles ->
+ * mpm_stage_begin.  Replaces nothing in the reference (single-process CPU). */
+int mpm_set_slab(mpm_ctx *ctx, const int *global_res, const int *offset, int ghost_bricks);
+int mpm_halo_buffers(mpm_ctx *ctx, int side, void **send_ids, void **send_data, void **recv_ids,
+                     void **recv_data, int64_t *capacity);
+int mpm_stage_begin(mpm_ctx *ctx, int nsub, int use_colliders);
+int mpm_stage_particles(mpm_ctx *ctx, int first);
+int mpm_stage_grid(mpm_ctx *ctx, int sub, int clear);
+int mpm_stage_end(mpm_ctx *ctx, int64_t *inverted);
+int mpm_halo_pack(mpm_ctx *ctx, int side, int64_t *count);
+int mpm_halo_unpack_add(mpm_ctx *ctx, int side, int64_t n);
+int mpm_halo_pack_vel(mpm_ctx *ctx, int side, int64_t *count);
+int mpm_halo_unpack_vel(mpm_ctx *ctx, int side, int64_t n);
+int mpm_extract_migrants(mpm_ctx *ctx, int own_lo, int own_hi, int64_t *n_lo, int64_t *n_hi,
+                         void **rows_lo, void **rows_hi, int64_t *rows_cap);
+int mpm_append_particles(mpm_ctx *ctx, const void *rows, int64_t m, int64_t rows_cap, int src_offset);
+int mpm_reserve(mpm_ctx *ctx, int64_t capacity);
+int mpm_download_ids(mpm_ctx *ctx, int32_t *ids, double *x);
+int mpm_device_copy(void *dst, const void *src, int64_t bytes);
+/* Slab windows identify particles by global id: */
+int mpm_set_ids(mpm_ctx *ctx, const int32_t *ids);
+int mpm_download_rows(mpm_ctx *ctx, int32_t *ids, double *x, double *v, double *F, double *C);
+
 /* ---- diagnostics -------------------------------------------------------- */
 /* update_collision_field (collision.py:244-272) over all nodes, current pose
  * row 0; dist (nx,ny,nz) f64, obj (nx,ny,nz) i32, cap = 2 theta. */

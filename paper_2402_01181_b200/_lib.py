@@ -34,7 +34,11 @@ EXPORTS = (
     "mpm_particle_count", "mpm_upload_grid", "mpm_download_grid", "mpm_set_colliders",
     "mpm_set_pose_table", "mpm_p2g", "mpm_grid_update", "mpm_g2p", "mpm_substeps",
     "mpm_collision_field", "mpm_has_nan", "mpm_launch_count", "mpm_host_alloc", "mpm_host_free",
-    "mpm_set_timing", "mpm_get_timing", "mpm_set_option",
+    "mpm_set_timing", "mpm_get_timing", "mpm_set_option", "mpm_set_slab", "mpm_halo_buffers",
+    "mpm_stage_begin", "mpm_stage_particles", "mpm_stage_grid", "mpm_stage_end", "mpm_halo_pack",
+    "mpm_halo_unpack_add", "mpm_halo_pack_vel", "mpm_halo_unpack_vel", "mpm_extract_migrants",
+    "mpm_append_particles", "mpm_reserve", "mpm_download_ids", "mpm_device_copy", "mpm_set_ids",
+    "mpm_download_rows",
 )
 
 
@@ -96,6 +100,25 @@ def lib():
     L.mpm_set_timing.argtypes = [_VP, ctypes.c_int]
     L.mpm_get_timing.argtypes = [_VP, _D]
     L.mpm_set_option.argtypes = [_VP, ctypes.c_char_p, ctypes.c_int]
+    _IP = ctypes.POINTER(ctypes.c_int)
+    _PP = ctypes.POINTER(_VP)
+    L.mpm_set_slab.argtypes = [_VP, _IP, _IP, ctypes.c_int]
+    L.mpm_halo_buffers.argtypes = [_VP, ctypes.c_int, _PP, _PP, _PP, _PP, _I64]
+    L.mpm_stage_begin.argtypes = [_VP, ctypes.c_int, ctypes.c_int]
+    L.mpm_stage_particles.argtypes = [_VP, ctypes.c_int]
+    L.mpm_stage_grid.argtypes = [_VP, ctypes.c_int, ctypes.c_int]
+    L.mpm_stage_end.argtypes = [_VP, _I64]
+    L.mpm_halo_pack.argtypes = [_VP, ctypes.c_int, _I64]
+    L.mpm_halo_unpack_add.argtypes = [_VP, ctypes.c_int, ctypes.c_int64]
+    L.mpm_halo_pack_vel.argtypes = [_VP, ctypes.c_int, _I64]
+    L.mpm_halo_unpack_vel.argtypes = [_VP, ctypes.c_int, ctypes.c_int64]
+    L.mpm_extract_migrants.argtypes = [_VP, ctypes.c_int, ctypes.c_int, _I64, _I64, _PP, _PP, _I64]
+    L.mpm_append_particles.argtypes = [_VP, _VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
+    L.mpm_reserve.argtypes = [_VP, ctypes.c_int64]
+    L.mpm_download_ids.argtypes = [_VP, _I32, _D]
+    L.mpm_device_copy.argtypes = [_VP, _VP, ctypes.c_int64]
+    L.mpm_set_ids.argtypes = [_VP, _I32]
+    L.mpm_download_rows.argtypes = [_VP, _I32, _D, _D, _D, _D]
     _lib = L
     return L
 

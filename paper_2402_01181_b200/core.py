@@ -166,6 +166,9 @@ class SimState:
 
     # ---------------------------------------------------------------- fields
     def _get(self, name: str) -> np.ndarray:
+        if getattr(self, "_slab_window", False):
+            from .errors import SimError
+            raise SimError("slab window state: read it through slab.SlabWindow.download()")
         if name in self._dev_newer:
             self._download((name,))
         self._host_dirty.add(name)
@@ -324,6 +327,8 @@ class SimState:
             raise StencilError("particle positions leave no room for the 3x3x3 stencil")
 
     def _sync_particles(self) -> None:
+        if getattr(self, "_slab_window", False):
+            return  # slab windows own their particle set on the device (migration)
         ctx = self._ctx
         n = len(self._h["x"])
         if n == 0:

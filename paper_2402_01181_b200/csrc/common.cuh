@@ -45,8 +45,14 @@ struct Params {
   float dx, inv_dx, dt;
   float gravity[3];
   float lo, hi[3];  // particle margin clamp (core.py:51-56), env-local
-  int env_res[3];   // nodes per environment tile (== res for one environment)
+  int env_res[3];   // nodes per environment tile (== gres for one environment)
   float env_ext[3]; // env_res * dx
+  // slab decomposition (config 5): this context's grid is the window of the
+  // global grid (gres nodes) starting at global node goff; particle positions
+  // on the device are window-local (global - goff * dx)
+  int goff[3];
+  int gres[3];
+  float goffx[3];   // goff * dx
   float stress_coef;  // -4 dt / dx^2 (kernels.py:207)
   float apic_coef;    // 4 / dx^2 (kernels.py:448)
   double dx64, dt64;

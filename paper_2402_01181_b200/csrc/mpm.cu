@@ -93,6 +93,24 @@ struct mpm_ctx {
   int* flag = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int fused_blocks = 0;
+
+  // slab decomposition window (config 5): global offset / resolution
+  int goff[3] = {0, 0, 0};
+  int gres[3] = {0, 0, 0};
+  int ghost_bricks = 1;
+  // halo buffers (device): per side {ids, data} for send and receive
+  int* h_send_ids[2] = {nullptr, nullptr};
+  float4* h_send_data[2] = {nullptr, nullptr};
+  int* h_recv_ids[2] = {nullptr, nullptr};
+  float4* h_recv_data[2] = {nullptr, nullptr};
+  int* h_local_ids[2] = {nullptr, nullptr};
+  int h_recv_n[2] = {0, 0};
+  long long h_cap = 0;  // records per buffer
+  int stage_nsub = 0, stage_col = 0;
+  // migration scratch
+  int* mflag = nullptr;
+  float* mig_rows[2] = {nullptr, nullptr};
+  long long mig_cap = 0;
   int gridop_blocks = 0;  // persistent grid sizes (SMs x resident CTAs)
   int gsA_blocks = 0, gsA0_blocks = 0, clear_blocks = 0, fused_only_blocks = 0;
 
@@ -246,7 +264,10 @@ Params make_params(mpm_ctx* ctx) {
     p.nbin[a] = ctx->nbin[a];
     p.gravity[a] = (float)c.gravity[a];
     const int et = c.env_tiles[a] > 1 ? c.env_tiles[a] : 1;
-    p.env_res[a] = c.res[a] / et;
+    p.goff[a] = ctx->goff[a];
+    p.gres[a] = ctx->gres[a] > 0 ? ctx->gres[a] : c.res[a];
+    p.goffx[a] = (float)(ctx->goff[a] * c.dx);
+    p.env_res[a] = p.gres[a] / et;
     p.env_ext[a] = (float)(p.env_res[a] * c.dx);
     double hd = (p.env_res[a] - 1.5 - 1.0e-7) * c.dx;
     float hf = (float)hd;
@@ -595,11 +616,11 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
   int rc = 0;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc) rc = alloc_grid(ctx);
-  if (!rc) rc = dalloc(ctx, &ctx->counters, 4);
+  if (!rc) rc = dalloc(ctx, &ctx->counters, 8);
   if (!rc) rc = dalloc(ctx, &ctx->inverted, 1);
   if (!rc) rc = dalloc(ctx, &ctx->flag, 1);
   if (!rc) rc = ensure_scan(ctx, ctx->nbins);
-  if (!rc && cudaMemsetAsync(ctx->counters, 0, 16, ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc && cudaMemsetAsync(ctx->counters, 0, 32, ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
@@ -643,7 +664,9 @@ int mpm_destroy(mpm_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   invalidate_graphs(ctx);
-  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box,
+  void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box, ctx->mflag, ctx->mig_rows[0], ctx->mig_rows[1], ctx->h_send_ids[0], ctx->h_send_ids[1],
+                  ctx->h_send_data[0], ctx->h_send_data[1], ctx->h_recv_ids[0], ctx->h_recv_ids[1], ctx->h_recv_data[0],
+                  ctx->h_recv_data[1], ctx->h_local_ids[0], ctx->h_local_ids[1],
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
                   ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag};
@@ -1145,6 +1168,327 @@ int mpm_get_timing(mpm_ctx* ctx, double* out) {
   out[12] = ctx->acc[10];
   out[13] = ctx->acc[11];
   for (double& a : ctx->acc) a = 0.0;
+  return 0;
+}
+
+// ---- slab decomposition (BASELINE config 5) ----------------------------
+
+int mpm_set_slab(mpm_ctx* ctx, const int* global_res, const int* offset, int ghost_bricks) {
+  if (!ctx || !global_res || !offset || ghost_bricks < 1) return fail(ctx, MPM_EINVAL, "set_slab: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  for (int a = 0; a < 3; ++a) {
+    if (offset[a] % 4 != 0) return fail(ctx, MPM_EINVAL, "set_slab: window offset must be a multiple of 4 nodes");
+    if (offset[a] < 0 || offset[a] + ctx->cfg.res[a] > global_res[a] + 4 * ghost_bricks)
+      return fail(ctx, MPM_EINVAL, "set_slab: window outside the global grid");
+  }
+  if (ctx->cfg.res[1] != global_res[1] || ctx->cfg.res[2] != global_res[2] || offset[1] || offset[2])
+    return fail(ctx, MPM_EINVAL, "set_slab: slabs split x only");
+  invalidate_graphs(ctx);
+  for (int a = 0; a < 3; ++a) {
+    ctx->goff[a] = offset[a];
+    ctx->gres[a] = global_res[a];
+  }
+  ctx->ghost_bricks = ghost_bricks;
+  const long long cap = (long long)ghost_bricks * ((ctx->cfg.res[1] + 3) / 4) * ((ctx->cfg.res[2] + 3) / 4);
+  if (cap > ctx->h_cap) {
+    for (int s = 0; s < 2; ++s) {
+      TRY(dalloc(ctx, &ctx->h_send_ids[s], (size_t)cap + 1));
+      TRY(dalloc(ctx, &ctx->h_send_data[s], (size_t)cap * 64));
+      TRY(dalloc(ctx, &ctx->h_recv_ids[s], (size_t)cap + 1));
+      TRY(dalloc(ctx, &ctx->h_recv_data[s], (size_t)cap * 64));
+      TRY(dalloc(ctx, &ctx->h_local_ids[s], (size_t)cap));
+    }
+    ctx->h_cap = cap;
+  }
+  return 0;
+}
+
+int mpm_halo_buffers(mpm_ctx* ctx, int side, void** send_ids, void** send_data, void** recv_ids, void** recv_data,
+                     int64_t* capacity) {
+  if (!ctx || side < 0 || side > 1 || !ctx->h_cap) return fail(ctx, MPM_ESTATE, "halo_buffers: call mpm_set_slab first");
+  if (send_ids) *send_ids = ctx->h_send_ids[side];
+  if (send_data) *send_data = ctx->h_send_data[side];
+  if (recv_ids) *recv_ids = ctx->h_recv_ids[side];
+  if (recv_data) *recv_data = ctx->h_recv_data[side];
+  if (capacity) *capacity = ctx->h_cap;
+  return 0;
+}
+
+int mpm_stage_begin(mpm_ctx* ctx, int nsub, int use_colliders) {
+  if (!ctx || nsub <= 0) return fail(ctx, MPM_EINVAL, "stage_begin: bad arguments");
+  TRY(need_particles(ctx));
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->cfg.deterministic) return fail(ctx, MPM_EINVAL, "stage driver: fast mode only");
+  ctx->stage_nsub = nsub;
+  ctx->stage_col = use_colliders && ctx->ncol > 0 && ctx->cfg.theta >= 0.0;
+  CK(cudaMemsetAsync(ctx->inverted, 0, sizeof(unsigned long long), ctx->stream));
+  TRY(ensure_gm_clean(ctx));
+  TRY(rebin(ctx));
+  return 0;
+}
+
+int mpm_stage_particles(mpm_ctx* ctx, int first) {
+  if (!ctx) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  TRY(launch_fused(ctx, first == 0));
+  return 0;
+}
+
+int mpm_stage_grid(mpm_ctx* ctx, int sub, int clear) {
+  if (!ctx) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  TRY(launch_grid_op(ctx, false, ctx->stage_col != 0, sub, clear != 0));
+  if (!clear) ctx->grid_dirty = 1;
+  return 0;
+}
+
+int mpm_stage_end(mpm_ctx* ctx, int64_t* inverted) {
+  if (!ctx) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  TRY(launch_g2p(ctx));
+  ctx->grid_dirty = 1;
+  ctx->grid_phase = 1;
+  return read_inverted(ctx, inverted);
+}
+
+int mpm_halo_pack(mpm_ctx* ctx, int side, int64_t* count) {
+  if (!ctx || side < 0 || side > 1 || !ctx->h_cap) return fail(ctx, MPM_ESTATE, "halo_pack: no slab");
+  CK(cudaSetDevice(ctx->dev));
+  int* cnt = ctx->counters + 2;
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int), ctx->stream));
+  Params p = make_params(ctx);
+  halo_pack_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, side, ctx->ghost_bricks, ctx->h_send_ids[side],
+                                                           ctx->h_send_data[side], cnt);
+  LAUNCHED();
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (h > ctx->h_cap) return fail(ctx, MPM_ESTATE, "halo_pack: overflow");
+  if (count) *count = h;
+  return 0;
+}
+
+int mpm_halo_unpack_add(mpm_ctx* ctx, int side, int64_t n) {
+  if (!ctx || side < 0 || side > 1 || n < 0 || n > ctx->h_cap) return fail(ctx, MPM_EINVAL, "halo_unpack_add: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  ctx->h_recv_n[side] = (int)n;
+  if (n == 0) return 0;
+  Params p = make_params(ctx);
+  halo_unpack_add_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_recv_ids[side], ctx->h_recv_data[side],
+                                                                 (int)n, ctx->h_local_ids[side]);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_halo_pack_vel(mpm_ctx* ctx, int side, int64_t* count) {
+  if (!ctx || side < 0 || side > 1) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const int n = ctx->h_recv_n[side];
+  if (count) *count = n;
+  if (n == 0) return 0;
+  Params p = make_params(ctx);
+  halo_pack_vel_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_local_ids[side], n, ctx->h_send_data[side]);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_halo_unpack_vel(mpm_ctx* ctx, int side, int64_t n) {
+  if (!ctx || side < 0 || side > 1 || n < 0 || n > ctx->h_cap) return fail(ctx, MPM_EINVAL, "halo_unpack_vel: bad arguments");
+  CK(cudaSetDevice(ctx->dev));
+  if (n == 0) return 0;
+  Params p = make_params(ctx);
+  // our packed ids of this side are still in h_send_ids[side]
+  halo_unpack_vel_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_send_ids[side], ctx->h_recv_data[side],
+                                                                 (int)n);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+// Remove particles whose global base cell x left [own_lo, own_hi) into two
+// device row buffers (low / high neighbour); returns their counts and buffer
+// pointers/capacity (rows: NF floats, material id, particle id; SoA by field).
+int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, int64_t* n_hi, void** rows_lo,
+                         void** rows_hi, int64_t* rows_cap) {
+  if (!ctx) return MPM_EINVAL;
+  TRY(need_particles(ctx));
+  CK(cudaSetDevice(ctx->dev));
+  invalidate_graphs(ctx);
+  const long long n = ctx->n;
+  if (!ctx->mflag || ctx->mig_cap < ctx->cap) {
+    TRY(dalloc(ctx, &ctx->mflag, (size_t)ctx->cap * 4));
+    for (int s = 0; s < 2; ++s) TRY(dalloc(ctx, &ctx->mig_rows[s], (size_t)ctx->cap * (NF + 2)));
+    ctx->mig_cap = ctx->cap;
+    TRY(ensure_scan(ctx, ctx->cap));
+  }
+  int* flag = ctx->mflag;
+  int* cls = flag + ctx->cap;
+  Params p = make_params(ctx);
+  migrant_flag_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, own_lo, own_hi, flag);
+  LAUNCHED();
+  int totals[3] = {0, 0, 0};
+  int* posv[3];
+  // class scans reuse the key/rank/lcell scratch
+  posv[0] = ctx->key;
+  posv[1] = ctx->rank;
+  posv[2] = ctx->lcell;
+  for (int c = 0; c < 3; ++c) {
+    flag_class_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(flag, c, cls, n);
+    LAUNCHED();
+    TRY(scan_exclusive(ctx, cls, posv[c], n));
+    int last_pos = 0, last_cls = 0;
+    CK(cudaMemcpyAsync(&last_pos, posv[c] + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&last_cls, cls + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    totals[c] = last_pos + last_cls;
+  }
+  const int nxt = ctx->cur ^ 1;
+  migrant_scatter_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
+      p, flag, posv[0], posv[1], posv[2], ctx->P[nxt], ctx->mat[nxt], ctx->orig[nxt], ctx->mig_rows[0], ctx->mig_rows[1],
+      ctx->mig_cap);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->cur = nxt;
+  ctx->n = totals[0];
+  if (n_lo) *n_lo = totals[1];
+  if (n_hi) *n_hi = totals[2];
+  if (rows_lo) *rows_lo = ctx->mig_rows[0];
+  if (rows_hi) *rows_hi = ctx->mig_rows[1];
+  if (rows_cap) *rows_cap = ctx->mig_cap;
+  return 0;
+}
+
+// Append m migrant rows (device buffer in the layout above, capacity rows_cap)
+// coming from a window whose global x offset is src_offset nodes.
+int mpm_append_particles(mpm_ctx* ctx, const void* rows, int64_t m, int64_t rows_cap, int src_offset) {
+  if (!ctx || m < 0) return MPM_EINVAL;
+  if (m == 0) return 0;
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->n + m > ctx->cap) return fail(ctx, MPM_ENOMEM, "append_particles: capacity exceeded (reserve with mpm_reserve)");
+  invalidate_graphs(ctx);
+  Params p = make_params(ctx);
+  const float dxs = (float)((src_offset - ctx->goff[0]) * ctx->cfg.dx);
+  append_rows_kernel<<<blocks_for(m, 256), 256, 0, ctx->stream>>>(p, (const float*)rows, m, rows_cap, ctx->n, dxs);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->n += m;
+  return 0;
+}
+
+// Grow particle capacity (keeps contents) so migrants can be appended.
+int mpm_reserve(mpm_ctx* ctx, int64_t cap) {
+  if (!ctx || cap <= ctx->cap) return 0;
+  CK(cudaSetDevice(ctx->dev));
+  invalidate_graphs(ctx);
+  float* P = nullptr;
+  int *mat = nullptr, *orig = nullptr;
+  TRY(dalloc(ctx, &P, (size_t)cap * NF));
+  TRY(dalloc(ctx, &mat, (size_t)cap));
+  TRY(dalloc(ctx, &orig, (size_t)cap));
+  for (int f = 0; f < NF; ++f)
+    CK(cudaMemcpyAsync(P + (size_t)f * cap, ctx->P[ctx->cur] + (size_t)f * ctx->cap, sizeof(float) * ctx->n,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(mat, ctx->mat[ctx->cur], sizeof(int) * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(orig, ctx->orig[ctx->cur], sizeof(int) * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(ctx->P[b]);
+    cudaFree(ctx->mat[b]);
+    cudaFree(ctx->orig[b]);
+    ctx->P[b] = nullptr;
+    ctx->mat[b] = nullptr;
+    ctx->orig[b] = nullptr;
+  }
+  ctx->P[0] = P;
+  ctx->mat[0] = mat;
+  ctx->orig[0] = orig;
+  TRY(dalloc(ctx, &ctx->P[1], (size_t)cap * NF));
+  TRY(dalloc(ctx, &ctx->mat[1], (size_t)cap));
+  TRY(dalloc(ctx, &ctx->orig[1], (size_t)cap));
+  ctx->cur = 0;
+  int* const* scratch[] = {&ctx->key, &ctx->rank, &ctx->lcell, &ctx->sidx, &ctx->slc, &ctx->bperm};
+  for (auto s : scratch) TRY(dalloc(ctx, const_cast<int**>(s), (size_t)cap));
+  ctx->work_cap = ctx->nbins + cap / MIN_CHUNK + 1;
+  TRY(dalloc(ctx, &ctx->work, (size_t)ctx->work_cap));
+  TRY(dalloc(ctx, &ctx->item_bounds, (size_t)ctx->work_cap));
+  TRY(dalloc(ctx, &ctx->item_bounds2, (size_t)ctx->work_cap));
+  ctx->bounds_a = ctx->item_bounds;
+  TRY(dalloc(ctx, &ctx->pay, (size_t)cap * NPAY));
+  TRY(dalloc(ctx, &ctx->item_box, (size_t)ctx->work_cap));
+  if (ctx->perm) {
+    cudaFree(ctx->perm);
+    cudaFree(ctx->payload);
+    ctx->perm = nullptr;
+    ctx->payload = nullptr;
+  }
+  ctx->cap = cap;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)cap * 24));
+  return 0;
+}
+
+// Replace the original-index slot of every particle by ids[original index]
+// (slab windows carry global particle ids; field readback is then by id).
+int mpm_set_ids(mpm_ctx* ctx, const int32_t* ids) {
+  if (!ctx || !ids) return MPM_EINVAL;
+  TRY(need_particles(ctx));
+  CK(cudaSetDevice(ctx->dev));
+  const long long n = ctx->n;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
+  int* sid = (int*)ctx->stage;
+  CK(cudaMemcpyAsync(sid, ids, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+  Params p = make_params(ctx);
+  set_ids_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, sid);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+// ids, x (global), v, F, C of every particle in device order.
+int mpm_download_rows(mpm_ctx* ctx, int32_t* ids, double* x, double* v, double* F, double* C) {
+  if (!ctx || !ids || !x || !v || !F || !C) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const long long n = ctx->n;
+  if (n <= 0) return 0;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 25 + 64));
+  Params p = make_params(ctx);
+  double* s = ctx->stage;
+  download_rows_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, s, s + 3 * n, s + 6 * n, s + 15 * n);
+  LAUNCHED();
+  download_ids_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, (int*)(s + 24 * n), s);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(ids, s + 24 * n, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(x, s, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(v, s + 3 * n, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(F, s + 6 * n, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(C, s + 15 * n, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+// Device-to-device copy (halo / migrant buffers between contexts or to
+// communication buffers).
+int mpm_device_copy(void* dst, const void* src, int64_t bytes) {
+  if (bytes <= 0) return 0;
+  return cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDefault) == cudaSuccess ? 0 : MPM_ECUDA;
+}
+
+// Particle ids (original indices) and global positions in device order.
+int mpm_download_ids(mpm_ctx* ctx, int32_t* ids, double* x) {
+  if (!ctx || !ids || !x) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const long long n = ctx->n;
+  if (n <= 0) return 0;
+  TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 4 + 64));
+  Params p = make_params(ctx);
+  double* sx = ctx->stage;
+  int* sid = (int*)(ctx->stage + 3 * n);
+  download_ids_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, sid, sx);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(ids, sid, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(x, sx, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 

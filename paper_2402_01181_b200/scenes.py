@@ -109,4 +109,15 @@ def c4_envs(n_envs: int = 1024, count: int = 30_000, res: int = 64, first_seed: 
     return EnvBatch(states, cols), mats, SimParams(), fns
 
 
-BUILDERS = {"c1": c1, "c2": c2, "c3": c3}
+def c5(count: int = 64_000_000, res: int = 1024, seed: int = 1):
+    """Config 5: a large tissue volume (0.4 x 0.1 x 0.4 m, ~3.7 particles per
+    cell at 1024^3) settling on the floor under gravity; slab-decomposed along x
+    across ranks by slab.split_state / bench.py --config c5."""
+    grid = Grid((res, res, res))
+    mats = _material()
+    spawn = sample_box((0.5, 0.065, 0.5), (0.4, 0.1, 0.4), count, seed=seed, grid=grid)
+    st = SimState.from_spawns(grid, [spawn], mats)
+    return st, mats, SimParams(rebin_interval=5), [], None
+
+
+BUILDERS = {"c1": c1, "c2": c2, "c3": c3, "c5": c5}

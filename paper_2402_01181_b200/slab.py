@@ -1,0 +1,373 @@
+"""Slab domain decomposition of one large scene (BASELINE config 5).
+
+The global grid is cut along x into windows owned by ranks (one GPU each).
+A particle belongs to the window that owns its base cell.  Each window's
+device context covers its owned x-range plus ``ghost_bricks`` 4-node brick
+layers on either side (mpm_set_slab); per substep:
+
+  1. particle stage (G2P(n) + F/stress + P2G(n+1)) into the local grid;
+  2. halo reduction: touched ghost bricks are packed sparsely (global brick
+     id + 64 nodes of momentum/mass) and sent to the owning neighbour, which
+     adds them into its bricks (mpm_halo_pack / mpm_halo_unpack_add);
+  3. grid op on the window (walls and tools in global coordinates);
+  4. velocity halo: the owner returns the velocities of exactly the bricks it
+     received, which overwrite the sender's ghost bricks;
+and at the end of each re-binning stretch particles whose base cell left the
+owned range migrate to the neighbour (mpm_extract_migrants /
+mpm_append_particles) before the next re-binning.  Ghost layers must cover the
+drift of one stretch (SimParams.rebin_interval substeps).
+
+Exchanges go through an ``Exchange`` object: ``LocalExchange`` copies device
+buffers between windows living in one process (single-GPU emulation and
+tests), ``TorchExchange`` uses torch.distributed point-to-point send/recv
+(NCCL over NVLink between GPUs; gloo on CPU for protocol tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib, core
+from .errors import ParameterError
+
+NF = 26          # particle float fields (csrc/common.cuh)
+ROWS = NF + 2    # + material id + particle id
+
+
+def partition(res_x: int, ranks: int, weights=None) -> list[tuple[int, int]]:
+    """Owned base-cell x ranges [lo, hi) per rank, multiples of 4 nodes."""
+    bricks = res_x // 4
+    if ranks < 1 or bricks < ranks:
+        raise ParameterError("too many slabs for the grid")
+    w = np.ones(ranks) if weights is None else np.asarray(weights, dtype=np.float64)
+    cuts = np.round(np.cumsum(w) / w.sum() * bricks).astype(int)
+    lo = 0
+    out = []
+    for r in range(ranks):
+        hi = int(cuts[r]) if r < ranks - 1 else bricks
+        hi = max(hi, lo + 1)
+        out.append((4 * lo, 4 * hi))
+        lo = hi
+    return out
+
+
+class SlabWindow:
+    """One rank's window: a SimState over the local grid + slab configuration."""
+
+    def __init__(self, grid: core.Grid, own: tuple[int, int], x, v, F, C, mass, vol0, mat, ids,
+                 ghost_bricks: int = 2, device: int | None = None, capacity: int | None = None):
+        self.global_grid = grid
+        self.own = own
+        g = 4 * ghost_bricks
+        nx, ny, nz = grid.resolution
+        self.offset = max(0, own[0] - g)
+        end = min(nx, own[1] + g)
+        res = (end - self.offset, ny, nz)
+        dx = grid.dx
+        local = core.Grid(res, (res[0] * dx, ny * dx, nz * dx))
+        xl = np.array(x, dtype=np.float64, copy=True)
+        xl[:, 0] -= self.offset * dx
+        self.state = core.SimState(local, xl, v, F, C, mass, vol0, mat, device=device)
+        self.ids = np.asarray(ids, dtype=np.int32)
+        self.ghost_bricks = ghost_bricks
+        self.capacity = capacity
+        self._configured = False
+
+    def configure(self, materials, params, colliders=None, rows=None):
+        st = self.state
+        theta = core._theta(st, params) if colliders else None
+        ctx = st._prepare(materials, params, theta)
+        if not self._configured:
+            L = _lib.lib()
+            gres = (ctypes.c_int * 3)(*self.global_grid.resolution)
+            off = (ctypes.c_int * 3)(self.offset, 0, 0)
+            ctx.call("mpm_set_slab", gres, off, self.ghost_bricks)
+            if self.capacity:
+                ctx.call("mpm_reserve", ctypes.c_int64(int(self.capacity)))
+            # the device keeps global particle ids in its original-index slots;
+            # from here on the window is read through download(), not SimState fields
+            ctx.call("mpm_set_ids", _lib.ptr(self.ids, _lib._I32))
+            st._slab_window = True
+            self._configured = True
+        if colliders:
+            st._packed_colliders(colliders, params)
+            st._upload_colliders()
+            st._upload_pose_rows(*rows)
+        return ctx
+
+    def buffers(self, side):
+        ctx = self.state._ctx
+        si, sd, ri, rd = (_lib._VP() for _ in range(4))
+        cap = ctypes.c_int64()
+        ctx.call("mpm_halo_buffers", side, ctypes.byref(si), ctypes.byref(sd), ctypes.byref(ri),
+                 ctypes.byref(rd), ctypes.byref(cap))
+        return si.value, sd.value, ri.value, rd.value, cap.value
+
+    def download(self):
+        """(ids, x global, v, F, C) of the particles currently owned, device order."""
+        ctx = self.state._ctx
+        n = int(_lib.lib().mpm_particle_count(ctx.h))
+        ids = np.empty(n, np.int32)
+        x, v = np.empty((n, 3)), np.empty((n, 3))
+        F, C = np.empty((n, 3, 3)), np.empty((n, 3, 3))
+        ctx.call("mpm_download_rows", _lib.ptr(ids, _lib._I32), _lib.ptr(x), _lib.ptr(v), _lib.ptr(F),
+                 _lib.ptr(C))
+        return ids, x, v, F, C
+
+
+class LocalExchange:
+    """All windows in this process (one GPU): exchanges are device copies."""
+
+    def __init__(self, windows):
+        self.w = windows
+
+    def halo(self, counts, phase):
+        """counts[r][side] records packed by window r toward `side`; phase 'mass'
+        delivers window r's side-1 records to r+1's side-0 receive buffers (and
+        side-0 to r-1's side-1), 'vel' replies in the opposite direction."""
+        L = _lib.lib()
+        recv = [[0, 0] for _ in self.w]
+        for r, win in enumerate(self.w):
+            for side, nb in ((0, r - 1), (1, r + 1)):
+                if nb < 0 or nb >= len(self.w):
+                    continue
+                m = counts[r][side]
+                si, sd, _, _, _ = win.buffers(side)
+                _, _, ri, rd, _ = self.w[nb].buffers(1 - side)
+                if phase == "mass":
+                    L.mpm_device_copy(ri, si, 4 * m)
+                L.mpm_device_copy(rd, sd, 16 * 64 * m)
+                recv[nb][1 - side] = m
+        return recv
+
+    def migrate(self, outgoing):
+        """outgoing[r] = {side: (ptr, m, cap)} -> appended to the neighbours."""
+        L = _lib.lib()
+        for r, out in enumerate(outgoing):
+            for side, (ptr, m, cap) in out.items():
+                nb = r - 1 if side == 0 else r + 1
+                if m == 0 or nb < 0 or nb >= len(self.w):
+                    continue
+                self.w[nb].state._ctx.call("mpm_append_particles", ptr, ctypes.c_int64(m),
+                                           ctypes.c_int64(cap), self.w[r].offset)
+
+
+class TorchExchange:
+    """torch.distributed point-to-point between neighbouring ranks (one window
+    per rank): NCCL on CUDA tensors, gloo on CPU tensors."""
+
+    def __init__(self, window, rank, world, device="cuda"):
+        self.win, self.rank, self.world, self.device = window, rank, world, device
+
+    def _sendrecv(self, send: dict, recv_shapes: dict, dtype):
+        import torch
+        import torch.distributed as dist
+        ops, out = [], {}
+        for nb, t in send.items():
+            ops.append(dist.P2POp(dist.isend, t, nb))
+        for nb, shape in recv_shapes.items():
+            out[nb] = torch.empty(shape, dtype=dtype, device=t.device if send else self.device)
+            ops.append(dist.P2POp(dist.irecv, out[nb], nb))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return out
+
+    def counts(self, mine: dict):
+        """Exchange int64 counts with the neighbours: {nb: count} -> {nb: count}."""
+        import torch
+        send = {nb: torch.tensor([c], dtype=torch.int64, device=self.device) for nb, c in mine.items()}
+        got = self._sendrecv(send, {nb: (1,) for nb in mine}, torch.int64)
+        return {nb: int(t.item()) for nb, t in got.items()}
+
+    def payload(self, mine: dict, recv_counts: dict, width: int, dtype):
+        """Exchange per-neighbour tensors of shape (count, width)."""
+        return self._sendrecv(mine, {nb: (recv_counts[nb], width) for nb in recv_counts}, dtype)
+
+
+def step_local(windows, exchange: LocalExchange, materials, params, colliders=None, pose_rows=None):
+    """One frame (params.substeps_per_frame substeps) of every window in this process."""
+    nsub = params.substeps_per_frame
+    L = int(params.rebin_interval)
+    inverted = 0
+    for win in windows:
+        win.configure(materials, params, colliders, pose_rows)
+    s = 0
+    while s < nsub:
+        span = min(L, nsub - s)
+        for win in windows:
+            win.state._ctx.call("mpm_stage_begin", nsub, int(bool(colliders)))
+        for t in range(span):
+            sub = s + t
+            for win in windows:
+                win.state._ctx.call("mpm_stage_particles", int(t == 0))
+            counts = []
+            for win in windows:
+                c = []
+                for side in (0, 1):
+                    n = ctypes.c_int64()
+                    win.state._ctx.call("mpm_halo_pack", side, ctypes.byref(n))
+                    c.append(n.value)
+                counts.append(c)
+            recv = exchange.halo(counts, "mass")
+            for r, win in enumerate(windows):
+                for side in (0, 1):
+                    win.state._ctx.call("mpm_halo_unpack_add", side, ctypes.c_int64(recv[r][side]))
+            for win in windows:
+                win.state._ctx.call("mpm_stage_grid", sub, int(sub != nsub - 1))
+            vcounts = []
+            for win in windows:
+                c = []
+                for side in (0, 1):
+                    n = ctypes.c_int64()
+                    win.state._ctx.call("mpm_halo_pack_vel", side, ctypes.byref(n))
+                    c.append(n.value)
+                vcounts.append(c)
+            # velocity replies travel back toward the sender of each brick
+            vrecv = exchange.halo(vcounts, "vel")
+            for r, win in enumerate(windows):
+                for side in (0, 1):
+                    win.state._ctx.call("mpm_halo_unpack_vel", side, ctypes.c_int64(vrecv[r][side]))
+        for win in windows:
+            inv = ctypes.c_int64()
+            win.state._ctx.call("mpm_stage_end", ctypes.byref(inv))
+            inverted += inv.value
+        outgoing = []
+        for win in windows:
+            nlo, nhi, plo, phi, cap = (ctypes.c_int64(), ctypes.c_int64(), _lib._VP(), _lib._VP(),
+                                       ctypes.c_int64())
+            win.state._ctx.call("mpm_extract_migrants", win.own[0], win.own[1], ctypes.byref(nlo),
+                                ctypes.byref(nhi), ctypes.byref(plo), ctypes.byref(phi), ctypes.byref(cap))
+            outgoing.append({0: (plo.value, nlo.value, cap.value), 1: (phi.value, nhi.value, cap.value)})
+        exchange.migrate(outgoing)
+        s += span
+    return inverted
+
+
+def gather(windows, n_total: int):
+    """Global x, v, F, C (particle-id order) from all windows of this process."""
+    x, v = np.full((n_total, 3), np.nan), np.full((n_total, 3), np.nan)
+    F, C = np.full((n_total, 3, 3), np.nan), np.full((n_total, 3, 3), np.nan)
+    for win in windows:
+        ids, xw, vw, Fw, Cw = win.download()
+        x[ids], v[ids], F[ids], C[ids] = xw, vw, Fw, Cw
+    return x, v, F, C
+
+
+def split_state(grid: core.Grid, x, v, F, C, mass, vol0, mat, ranks: int, ghost_bricks: int = 2,
+                device: int | None = None, capacity_factor: float = 1.5):
+    """Cut a global particle set into slab windows (base-cell ownership)."""
+    dx = grid.dx
+    base = np.floor(np.asarray(x)[:, 0] / dx - 0.5).astype(np.int64)
+    parts = partition(grid.resolution[0], ranks)
+    wins = []
+    ids = np.arange(len(x), dtype=np.int32)
+    for own in parts:
+        sel = (base >= own[0]) & (base < own[1])
+        cap = int(max(16, capacity_factor * sel.sum() + 1024))
+        wins.append(SlabWindow(grid, own, x[sel], v[sel], F[sel], C[sel], mass[sel], vol0[sel], mat[sel],
+                               ids[sel], ghost_bricks=ghost_bricks, device=device, capacity=cap))
+    return wins
+
+
+# ---------------------------------------------------------------------------
+# one window per rank (torchrun): exchanges over torch.distributed
+# ---------------------------------------------------------------------------
+
+def _dev_tensor(nbytes_or_shape, dtype, device):
+    import torch
+    return torch.empty(nbytes_or_shape, dtype=dtype, device=device)
+
+
+def _neighbours(rank, world):
+    return {side: nb for side, nb in ((0, rank - 1), (1, rank + 1)) if 0 <= nb < world}
+
+
+def _halo_exchange(win: SlabWindow, ex: TorchExchange, counts: dict, with_ids: bool):
+    """Send our packed side buffers to the neighbours, receive theirs into our
+    receive buffers.  counts: {side: records}.  Returns {side: records received}."""
+    import torch
+    L = _lib.lib()
+    nbs = _neighbours(ex.rank, ex.world)
+    got = ex.counts({nb: counts[side] for side, nb in nbs.items()})
+    recv = {}
+    for name, width, dtype, elem in ((("ids", 1, torch.int32, 4),) if with_ids else ()) + (("data", 256, torch.float32, 4),):
+        send = {}
+        for side, nb in nbs.items():
+            si, sd, _, _, _ = win.buffers(side)
+            t = _dev_tensor((counts[side], width), dtype, ex.device)
+            L.mpm_device_copy(t.data_ptr(), si if name == "ids" else sd, counts[side] * width * elem)
+            send[nb] = t
+        out = ex.payload(send, got, width, dtype)
+        for side, nb in nbs.items():
+            _, _, ri, rd, _ = win.buffers(side)
+            n = got[nb]
+            L.mpm_device_copy(ri if name == "ids" else rd, out[nb].data_ptr(), n * width * elem)
+            recv[side] = n
+        torch.cuda.synchronize()
+    return {side: recv.get(side, 0) for side in (0, 1)}
+
+
+def step_distributed(win: SlabWindow, ex: TorchExchange, materials, params, colliders=None, pose_rows=None):
+    """One frame for this rank's window; halos/migrants travel over torch.distributed."""
+    import torch
+    L = _lib.lib()
+    ctx = win.configure(materials, params, colliders, pose_rows)
+    nsub = params.substeps_per_frame
+    span_max = int(params.rebin_interval)
+    inverted = 0
+    s = 0
+    while s < nsub:
+        span = min(span_max, nsub - s)
+        ctx.call("mpm_stage_begin", nsub, int(bool(colliders)))
+        for t in range(span):
+            sub = s + t
+            ctx.call("mpm_stage_particles", int(t == 0))
+            counts = {}
+            for side in (0, 1):
+                n = ctypes.c_int64()
+                ctx.call("mpm_halo_pack", side, ctypes.byref(n))
+                counts[side] = n.value
+            recv = _halo_exchange(win, ex, counts, with_ids=True)
+            for side in (0, 1):
+                ctx.call("mpm_halo_unpack_add", side, ctypes.c_int64(recv[side]))
+            ctx.call("mpm_stage_grid", sub, int(sub != nsub - 1))
+            vcounts = {}
+            for side in (0, 1):
+                n = ctypes.c_int64()
+                ctx.call("mpm_halo_pack_vel", side, ctypes.byref(n))
+                vcounts[side] = n.value
+            vrecv = _halo_exchange(win, ex, vcounts, with_ids=False)
+            for side in (0, 1):
+                ctx.call("mpm_halo_unpack_vel", side, ctypes.c_int64(vrecv[side]))
+        inv = ctypes.c_int64()
+        ctx.call("mpm_stage_end", ctypes.byref(inv))
+        inverted += inv.value
+        # migration
+        nlo, nhi, plo, phi, cap = (ctypes.c_int64(), ctypes.c_int64(), _lib._VP(), _lib._VP(), ctypes.c_int64())
+        ctx.call("mpm_extract_migrants", win.own[0], win.own[1], ctypes.byref(nlo), ctypes.byref(nhi),
+                 ctypes.byref(plo), ctypes.byref(phi), ctypes.byref(cap))
+        nbs = _neighbours(ex.rank, ex.world)
+        mine = {0: (plo.value, nlo.value), 1: (phi.value, nhi.value)}
+        got = ex.counts({nb: mine[side][1] for side, nb in nbs.items()})
+        send = {}
+        for side, nb in nbs.items():
+            ptr, m = mine[side]
+            t = _dev_tensor((ROWS, m), torch.float32, ex.device)
+            for f in range(ROWS):
+                L.mpm_device_copy(t.data_ptr() + 4 * f * m, ptr + 4 * f * cap.value, 4 * m)
+            send[nb] = t
+        ops_out = ex._sendrecv({nb: t.reshape(-1) for nb, t in send.items()},
+                               {nb: (ROWS * got[nb],) for nb in got}, torch.float32)
+        torch.cuda.synchronize()
+        offsets = ex.counts({nb: win.offset for nb in nbs.values()})
+        for nb, t in ops_out.items():
+            m = got[nb]
+            if m:
+                ctx.call("mpm_append_particles", _lib._VP(t.data_ptr()), ctypes.c_int64(m), ctypes.c_int64(m),
+                         offsets[nb])
+        torch.cuda.synchronize()
+        s += span
+    return inverted

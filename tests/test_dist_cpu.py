@@ -58,3 +58,48 @@ def test_shard_and_tiles_single_process():
         t = tile_shape(n)
         assert t[0] * t[1] * t[2] >= n
         assert t[0] * t[1] * t[2] < 2 * n + 2
+
+
+def _exchange_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from paper_2402_01181_b200.slab import TorchExchange, _neighbours
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ex = TorchExchange(None, rank, world, device="cpu")
+        nbs = _neighbours(rank, world)
+        # halo-record counts and payloads: rank r sends (r+1)*(nb+1) rows of value 100r+nb
+        counts = ex.counts({nb: (rank + 1) * (nb + 1) for nb in nbs.values()})
+        send = {nb: torch.full(((rank + 1) * (nb + 1), 3), 100.0 * rank + nb) for nb in nbs.values()}
+        got = ex.payload(send, counts, 3, torch.float32)
+        out[rank] = {nb: (counts[nb], float(got[nb][0, 0]) if counts[nb] else None, tuple(got[nb].shape))
+                     for nb in nbs.values()}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_slab_neighbour_exchange_protocol():
+    """The slab driver's point-to-point protocol (counts, then payloads) pairs
+    every rank with its x-neighbours and delivers shapes/values intact."""
+    world = 3
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_exchange_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        for nb, (cnt, val, shape) in out[r].items():
+            assert cnt == (nb + 1) * (r + 1)
+            assert val == 100.0 * nb + r
+            assert shape == (cnt, 3)
+    assert set(out[0]) == {1} and set(out[1]) == {0, 2} and set(out[2]) == {1}
+
+
+def test_slab_partition():
+    from paper_2402_01181_b200.slab import partition
+    for res, ranks in ((1024, 8), (64, 3), (256, 2)):
+        parts = partition(res, ranks)
+        assert parts[0][0] == 0 and parts[-1][1] == res
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        assert all(lo % 4 == 0 and hi % 4 == 0 for lo, hi in parts)
+        widths = [hi - lo for lo, hi in parts]
+        assert max(widths) - min(widths) <= 4
