@@ -272,6 +272,8 @@ def run_ours(args, rank, world, local_rank):
         workload = (f"{args.config}: {st.particle_count} particles/GPU, {st.grid.resolution[0]}^3 grid, "
                     f"{len(cols)} tool(s)" + (" pressing 3 cm at 0.5 m/s then holding" if args.config == "c3" else "")
                     + ", 25 substeps per step")
+    if args.rebin:
+        params.rebin_interval = args.rebin
     n = st.particle_count
     nsub = params.substeps_per_frame
     L = _lib.lib()
@@ -466,6 +468,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--envs", type=int, default=1024, help="c4: environments over all ranks")
+    ap.add_argument("--rebin", type=int, default=None, help="override SimParams.rebin_interval")
     ap.add_argument("--particles", type=int, default=None)
     ap.add_argument("--cpu-substeps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -16,7 +16,7 @@ import numpy as np
 from .errors import ParameterError, SimError, StencilError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsoftmpm_b200.so")
+LIB_PATH = os.environ.get("SOFTMPM_LIB") or os.path.join(_HERE, "libsoftmpm_b200.so")
 _lib = None
 
 MPM_OK, MPM_EINVAL, MPM_ENOMEM, MPM_ECUDA, MPM_ESTATE, MPM_ESTENCIL = 0, -1, -2, -3, -4, -5

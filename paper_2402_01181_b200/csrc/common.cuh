@@ -22,10 +22,21 @@ constexpr int BRICK_SHIFT = 2;            // 4^3 nodes per layout brick
 constexpr int BRICK_NODES = 64;
 constexpr int BIN = 8;                    // particle bin edge (cells)
 constexpr int BIN_SHIFT = 3;
-constexpr int MARGIN = 2;                 // tile margin for particles drifting out of their bin
+#ifndef MPM_MARGIN
+#define MPM_MARGIN 2
+#endif
+constexpr int MARGIN = MPM_MARGIN;        // tile margin for particles drifting out of their bin
 constexpr int TILE = BIN + 2 + 2 * MARGIN;  // 14 nodes per tile edge
 constexpr int TILE_NODES = TILE * TILE * TILE;
 constexpr int FUSED_THREADS = 256;      // stage A (g2p_stress_kernel)
+#ifndef MPM_FUSED_THREADS
+#define MPM_FUSED_THREADS 256
+#endif
+#ifndef MPM_FUSED_MINB
+#define MPM_FUSED_MINB 2
+#endif
+constexpr int FUSED_K_THREADS = MPM_FUSED_THREADS;  // fused steady-state kernel
+constexpr int FUSED_MIN_BLOCKS = MPM_FUSED_MINB;
 constexpr int P2G_THREADS = 256;        // stage B (p2g_tile_kernel)
 constexpr int P2G_MIN_BLOCKS = 3;
 constexpr int NPAY = 13;                // payload floats per particle: m v (3), A (9), m

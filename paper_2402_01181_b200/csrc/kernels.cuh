@@ -413,13 +413,15 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
         tv.hi[a] = (pb >> (12 + 4 * a)) & 15;
       }
       // 2-D mapping over the (y, z) node box, loop along x
-      const int ty = tv.lo[1] + (threadIdx.x >> 4), tz = tv.lo[2] + (threadIdx.x & 15);
-      const int gj = tv.org[1] + ty, gk = tv.org[2] + tz;
-      if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
-        const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
-                             ((gj & 3) << 2) + (gk & 3);
-        const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-        load_vtile_column(p, vtile, tv.org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
+      for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+        const int ty = tv.lo[1] + (c >> 4), tz = tv.lo[2] + (c & 15);
+        const int gj = tv.org[1] + ty, gk = tv.org[2] + tz;
+        if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
+          const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                               ((gj & 3) << 2) + (gk & 3);
+          const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+          load_vtile_column(p, vtile, tv.org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
+        }
       }
       __syncthreads();
     }
@@ -672,7 +674,7 @@ __device__ __forceinline__ float sel4(bool r1, bool r2, float v0, float v1, floa
   return r2 ? b : a;
 }
 
-__global__ void __launch_bounds__(FUSED_THREADS, 2) fused_kernel(Params p, const float4* __restrict__ bounds_in,
+__global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, const float4* __restrict__ bounds_in,
                                                                  float4* __restrict__ bounds_out,
                                                                  int* __restrict__ item_box) {
   extern __shared__ float smem[];
@@ -712,13 +714,15 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) fused_kernel(Params p, const
         tv.lo[a] = (pb >> (4 * a)) & 15;
         tv.hi[a] = (pb >> (12 + 4 * a)) & 15;
       }
-      const int ty = tv.lo[1] + (threadIdx.x >> 4), tz = tv.lo[2] + (threadIdx.x & 15);
-      const int gj = org[1] + ty, gk = org[2] + tz;
-      if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
-        const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
-                             ((gj & 3) << 2) + (gk & 3);
-        const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-        load_vtile_column(p, vtile, org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
+      for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+        const int ty = tv.lo[1] + (c >> 4), tz = tv.lo[2] + (c & 15);
+        const int gj = org[1] + ty, gk = org[2] + tz;
+        if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
+          const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                               ((gj & 3) << 2) + (gk & 3);
+          const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+          load_vtile_column(p, vtile, org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
+        }
       }
     }
     for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;

@@ -485,7 +485,7 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
   {
     TimedRegion tr(ctx, 5);
-    fused_kernel<<<ctx->fused_only_blocks, FUSED_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
+    fused_kernel<<<ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
         p, ctx->item_bounds, ctx->item_bounds2, ctx->item_box);
     LAUNCHED();
   }
@@ -648,7 +648,7 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
     ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
-    ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_THREADS, sizeof(float) * 7 * TILE_NODES);
+    ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   }
   if (rc) {
