@@ -674,6 +674,46 @@ __device__ __forceinline__ float sel4(bool r1, bool r2, float v0, float v1, floa
   return r2 ? b : a;
 }
 
+// Decode a work item: tile origin and the velocity-tile box (the base cells it
+// scattered from in the previous substep, item_box).
+__device__ __forceinline__ void fused_item_geometry(const Params& p, const int4 item, int packed_box, TileVel& tv) {
+  const int bin = item.x;
+  const int bz = bin % p.nbin[2];
+  const int by = (bin / p.nbin[2]) % p.nbin[1];
+  const int bx = bin / (p.nbin[1] * p.nbin[2]);
+  tv.org[0] = bx * BIN - MARGIN;
+  tv.org[1] = by * BIN - MARGIN;
+  tv.org[2] = bz * BIN - MARGIN;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    tv.lo[a] = (packed_box >> (4 * a)) & 15;
+    tv.hi[a] = (packed_box >> (12 + 4 * a)) & 15;
+  }
+}
+
+// Fill the velocity tile of an item and its channel scales (called by the
+// whole CTA in the phase before the item's scatter).
+__device__ __forceinline__ void fused_item_prologue(const Params& p, const TileVel& tv, float* vtile, const int4 item,
+                                                    const float4 bd, float* scale_slot) {
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+    const int ty = tv.lo[1] + (c >> 4), tz = tv.lo[2] + (c & 15);
+    const int gj = tv.org[1] + ty, gk = tv.org[2] + tz;
+    if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
+      const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                           ((gj & 3) << 2) + (gk & 3);
+      const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+      load_vtile_column(p, vtile, tv.org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
+    }
+  }
+  if (threadIdx.x < 4) {
+    const float b[4] = {bd.x * BOUND_SAFETY, bd.y * BOUND_SAFETY, bd.z * BOUND_SAFETY, bd.w};
+    scale_slot[threadIdx.x] = channel_scale(b[threadIdx.x], item.w);
+  }
+}
+
+// Fused steady-state kernel, two barriers per item: [B] after the scatter
+// (tile complete) and [A] after the flush of this item overlapped with the
+// velocity-tile load of the CTA's next item (disjoint shared-memory regions).
 __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, const float4* __restrict__ bounds_in,
                                                                  float4* __restrict__ bounds_out,
                                                                  int* __restrict__ item_box) {
@@ -694,49 +734,25 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   for (int s = 0; s < 4; ++s) off[s] = ((s + rot) & 3) * TILE_NODES;
   unsigned inverted = 0;
   int par = 0;
+  if (blockIdx.x < nwork) {
+    TileVel tv0;
+    const int4 it0 = p.work[blockIdx.x];
+    fused_item_geometry(p, it0, item_box[blockIdx.x], tv0);
+    fused_item_prologue(p, tv0, vtile, it0, bounds_in[blockIdx.x], scale_s[0]);
+  }
+  __syncthreads();  // [A] first velocity tile + scales ready
   for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, par ^= 1) {
     int* box = boxes[par];
     const int4 item = p.work[wi];
-    const int bin = item.x;
-    const int bz = bin % p.nbin[2];
-    const int by = (bin / p.nbin[2]) % p.nbin[1];
-    const int bx = bin / (p.nbin[1] * p.nbin[2]);
-    const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
     TileVel tv;
     tv.t = vtile;
-    tv.org[0] = org[0];
-    tv.org[1] = org[1];
-    tv.org[2] = org[2];
-    {
-      const int pb = item_box[wi];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        tv.lo[a] = (pb >> (4 * a)) & 15;
-        tv.hi[a] = (pb >> (12 + 4 * a)) & 15;
-      }
-      for (int c = threadIdx.x; c < 256; c += blockDim.x) {
-        const int ty = tv.lo[1] + (c >> 4), tz = tv.lo[2] + (c & 15);
-        const int gj = org[1] + ty, gk = org[2] + tz;
-        if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
-          const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
-                               ((gj & 3) << 2) + (gk & 3);
-          const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-          load_vtile_column(p, vtile, org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
-        }
-      }
-    }
+    fused_item_geometry(p, item, item_box[wi], tv);
+    const int* org = tv.org;
+    const float4 bd = bounds_in[wi];
+    const float B[4] = {bd.x * BOUND_SAFETY, bd.y * BOUND_SAFETY, bd.z * BOUND_SAFETY, bd.w};
+    // previous item's brick flags / box buffer (its flush ended before the last [A])
     for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
-    float B[4];
-    {
-      const float4 bd = bounds_in[wi];
-      B[0] = bd.x * BOUND_SAFETY;
-      B[1] = bd.y * BOUND_SAFETY;
-      B[2] = bd.z * BOUND_SAFETY;
-      B[3] = bd.w;
-    }
-    if (threadIdx.x < 4) scale_s[par][threadIdx.x] = channel_scale(B[threadIdx.x], item.w);
-    __syncthreads();  // [1] velocity tile + scales ready; previous flush complete
     const float S[4] = {scale_s[par][0], scale_s[par][1], scale_s[par][2], scale_s[par][3]};
     float sc[4];
 #pragma unroll
@@ -828,7 +844,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
         atomicMax(&box[3 + a], h);
       }
     }
-    __syncthreads();  // [2] scatter complete
+    __syncthreads();  // [B] scatter complete; velocity tile free
     const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
     if (threadIdx.x == 0)
       item_box[wi] = x1 - 2 < x0 ? 0x00000FFF
@@ -860,7 +876,15 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
         if (atomicExch(&touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz], 1) == 0) mark_brick(p, idx);
       }
     }
-    __syncthreads();  // [3] flush complete: tile zero, velocity tile free
+    // overlapped with the flush: the CTA's next item's velocity tile + scales
+    const int nxt = wi + gridDim.x;
+    if (nxt < nwork) {
+      TileVel tn;
+      const int4 itn = p.work[nxt];
+      fused_item_geometry(p, itn, item_box[nxt], tn);
+      fused_item_prologue(p, tn, vtile, itn, bounds_in[nxt], scale_s[par ^ 1]);
+    }
+    __syncthreads();  // [A] flush complete (tile zero), next velocity tile ready
   }
   warp_count_add(p.inverted, inverted);
 }

@@ -134,6 +134,7 @@ struct mpm_ctx {
   std::vector<cudaEvent_t> event_pool;
   double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
+  int items_per_sm = 8;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
 };
 
 namespace {
@@ -448,7 +449,7 @@ int rebin(mpm_ctx* ctx) {
   LAUNCHED();
   ctx->cur = nxt;
   // ~4 items per SM at least: small scenes split bins, large ones keep whole bins
-  const int chunk = (int)std::max<long long>(MIN_CHUNK, std::min<long long>(CHUNK, ctx->n / (4LL * ctx->sms)));
+  const int chunk = (int)std::max<long long>(MIN_CHUNK, std::min<long long>(CHUNK, ctx->n / ((long long)ctx->items_per_sm * ctx->sms)));
   make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(
       ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, ctx->counters + 1, chunk);
   LAUNCHED();
@@ -632,6 +633,8 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
       ctx->split_mode = e && e[0] == '1';
       const char* g = getenv("SOFTMPM_GRAPHS");
       ctx->graphs_on = !(g && g[0] == '0');
+      const char* ips = getenv("SOFTMPM_ITEMS_PER_SM");
+      if (ips && atoi(ips) > 0) ctx->items_per_sm = atoi(ips);
     }
     cudaFuncSetAttribute(g2p_stress_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(float) * 6 * TILE_NODES));
