@@ -451,62 +451,42 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
   warp_count_add(p.inverted, inverted);
 }
 
-// Per-thread rotated view of the payload rows: in atomic slot s lane l
-// writes channel (s + l) & 3 (0..2 = m v components, 3 = mass).  Every
-// channel is written in the uniform form wt * (b + A_row . dp) (mass: b = m,
-// A row = 0), so up to four lanes of the same cell -- the common case in
-// cell-sorted order -- target four different channel arrays (different
-// addresses and banks) in every ATOMS instead of serializing on one address.
-struct RotRows {
-  const float* b[4];  // pay row of b for slot s
-  const float* a[4];  // first pay row of the A row for slot s
-  float amul[4];      // 1, or 0 for the mass slot
-  int off[4];         // channel offset in the SoA tile
-  int ch[4];
-};
-
-__device__ __forceinline__ RotRows make_rot_rows(const Params& p, const float* pay, int rot) {
-  RotRows rr;
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int ch = (s + rot) & 3;
-    rr.ch[s] = ch;
-    rr.b[s] = pay + (long long)(ch < 3 ? ch : 12) * p.cap;
-    rr.a[s] = pay + (long long)(ch < 3 ? 3 + 3 * ch : 3) * p.cap;
-    rr.amul[s] = ch < 3 ? 1.0f : 0.0f;
-    rr.off[s] = ch * TILE_NODES;
-  }
-  return rr;
+// Scatter one particle's payload into the int32 tile with lane-rotated
+// channels: slot s of a lane adds channel (s + rot) & 3 at tile + off[s], so
+// the 4 lanes of a quad hit 4 different channel planes at each step -- the
+// common case of several lanes on the same cell does not collide on one word.
+// Every channel has the uniform form wt * (b + A_row . dp) (mass: b = m, zero
+// A row); sel4 picks the rotated row values.
+__device__ __forceinline__ float sel4(bool r1, bool r2, float v0, float v1, float v2, float v3) {
+  const float a = r1 ? v1 : v0;
+  const float b = r1 ? v3 : v2;
+  return r2 ? b : a;
 }
 
-// Tile scatter of particle i (base cell b, fraction f) with rotated rows.
-__device__ __forceinline__ void p2g_scatter_rot(const Params& p, int* tile, const int org[3],
-                                                const RotRows& rr, const float sc[4], long long i,
-                                                const int b[3], const float f[3]) {
+__device__ __forceinline__ void tile_scatter_rot(int* tile, const int off[4], bool r1, bool r2, const float sc[4],
+                                                 const Payload& q, const int lc[3], float dx) {
+  const float chb[4] = {q.mv[0], q.mv[1], q.mv[2], q.m};
+  float bs[4], as[4][3];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    bs[s] = sel4(r1, r2, chb[s & 3], chb[(s + 1) & 3], chb[(s + 2) & 3], chb[(s + 3) & 3]) * sc[s];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float ca[4] = {q.A[c], q.A[3 + c], q.A[6 + c], 0.0f};
+      as[s][c] = sel4(r1, r2, ca[s & 3], ca[(s + 1) & 3], ca[(s + 2) & 3], ca[(s + 3) & 3]) * sc[s];
+    }
+  }
   float w[3][3], dxs[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const float t0 = 1.5f - f[a], t1 = f[a] - 1.0f, t2 = f[a] - 0.5f;
+    const float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
     w[a][0] = 0.5f * (t0 * t0);
     w[a][1] = 0.75f - t1 * t1;
     w[a][2] = 0.5f * (t2 * t2);
 #pragma unroll
-    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - f[a]) * p.dx;
+    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * dx;
   }
-  float bs[4], ax[3][4], ay[3][4], az[3][4];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    bs[s] = rr.b[s][i] * sc[s];
-    const float sa = sc[s] * rr.amul[s];
-    const float a0 = rr.a[s][i] * sa, a1 = rr.a[s][p.cap + i] * sa, a2 = rr.a[s][2 * p.cap + i] * sa;
-#pragma unroll
-    for (int o = 0; o < 3; ++o) {
-      ax[o][s] = a0 * dxs[0][o];
-      ay[o][s] = a1 * dxs[1][o];
-      az[o][s] = a2 * dxs[2][o];
-    }
-  }
-  const int base = ((b[0] - org[0]) * TILE + (b[1] - org[1])) * TILE + (b[2] - org[2]);
+  const int base = (lc[0] * TILE + lc[1]) * TILE + lc[2];
 #pragma unroll
   for (int ii = 0; ii < 3; ++ii) {
 #pragma unroll
@@ -514,15 +494,72 @@ __device__ __forceinline__ void p2g_scatter_rot(const Params& p, int* tile, cons
       const float wij = w[0][ii] * w[1][j];
       float bij[4];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) bij[s] = bs[s] + ax[ii][s] + ay[j][s];
+      for (int s = 0; s < 4; ++s) bij[s] = bs[s] + as[s][0] * dxs[0][ii] + as[s][1] * dxs[1][j];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float wt = wij * w[2][k];
         int* t = tile + base + (ii * TILE + j) * TILE + k;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) atomicAdd(t + rr.off[s], fixq(wt, bij[s] + az[k][s]));
+        for (int s = 0; s < 4; ++s) atomicAdd(t + off[s], fixq(wt, bij[s] + as[s][2] * dxs[2][k]));
       }
     }
+  }
+}
+
+// Flush an int32 fixed-point tile's node box [x0,x1]x[y0,y1]x[z0,z1] (tile
+// coordinates) into gm: one REDG.F32x4 per non-empty node, the box re-zeroed,
+// and every brick overlapping the box marked active.  The whole CTA shares the
+// work as (x-segment of SEG nodes, y, z) units, z fastest so consecutive lanes
+// hit consecutive float4s of a brick row; a segment's 4*SEG LDS are issued
+// before any of its REDGs.  Box nodes are inside the grid by construction
+// (bases are clamped to [0, res-3]), so there are no bounds checks.
+template <int SEG>
+__device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int* org, int x0, int x1, int y0, int y1,
+                                           int z0, int z1, const float inv[4]) {
+  if (x1 < x0 + 2) return;  // empty box (every particle fell back to gm)
+  const int nx = x1 - x0 + 1, ny = y1 - y0 + 1, nz = z1 - z0 + 1;
+  const int nyz = ny * nz, units = nyz * ((nx + SEG - 1) / SEG);
+  const float rz = 1.0f / (float)nz, ryz = 1.0f / (float)nyz;  // exact quotients for u < 2^10
+  const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
+  for (int u = threadIdx.x; u < units; u += blockDim.x) {
+    const int seg = (int)(((float)u + 0.5f) * ryz);
+    const int r = u - seg * nyz;
+    const int dy = (int)(((float)r + 0.5f) * rz);
+    const int ty = y0 + dy, tz = z0 + r - dy * nz, xs = x0 + SEG * seg;
+    const int gj = org[1] + ty, gk = org[2] + tz;
+    const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
+                         ((gj & 3) << 2) + (gk & 3);
+    int4 a[SEG];
+#pragma unroll
+    for (int k = 0; k < SEG; ++k) {
+      const int t = ((xs + k) * TILE + ty) * TILE + tz;
+      a[k] = xs + k <= x1 ? make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t], tile[3 * TILE_NODES + t])
+                          : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < SEG; ++k) {
+      if (xs + k > x1) continue;
+      const int t = ((xs + k) * TILE + ty) * TILE + tz;
+      tile[t] = 0;
+      tile[TILE_NODES + t] = 0;
+      tile[2 * TILE_NODES + t] = 0;
+      tile[3 * TILE_NODES + t] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < SEG; ++k) {
+      if ((a[k].x | a[k].y | a[k].z | a[k].w) == 0) continue;
+      const int gi = org[0] + xs + k;
+      atomicAdd(p.gm + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4),
+                make_float4((float)a[k].x * inv[0], (float)a[k].y * inv[1], (float)a[k].z * inv[2],
+                            (float)a[k].w * inv[3]));
+    }
+  }
+  const int bx0 = (org[0] + x0) >> BRICK_SHIFT, by0 = (org[1] + y0) >> BRICK_SHIFT, bz0 = (org[2] + z0) >> BRICK_SHIFT;
+  const int nbx = ((org[0] + x1) >> BRICK_SHIFT) - bx0 + 1, nby = ((org[1] + y1) >> BRICK_SHIFT) - by0 + 1,
+            nbz = ((org[2] + z1) >> BRICK_SHIFT) - bz0 + 1;
+  for (int t = threadIdx.x; t < nbx * nby * nbz; t += blockDim.x) {
+    const int bz = t % nbz, by = (t / nbz) % nby, bx = t / (nbz * nby);
+    mark_brick(p, ((long long)((bx0 + bx) * p.nb[1] + by0 + by) * p.nb[2] + bz0 + bz) << 6);
   }
 }
 
@@ -533,21 +570,23 @@ __device__ __forceinline__ void p2g_scatter_rot(const Params& p, int* tile, cons
 // FFMA magic range and no node sum can leave int32).  Particles whose stencil
 // leaves the tile go straight to gm with float REDG.F32x4.  The flush walks
 // only the touched node box, rescales exactly, issues one REDG.F32x4 per
-// non-empty node, re-zeroes the tile, marks each touched 4^3 brick active once
-// (first toucher via a shared flag) and records the box for the next
+// non-empty node, re-zeroes the tile, marks the box's 4^3 bricks active
+// (flush_tile) and records the box for the next
 // substep's G2P tile.  Two barriers per item.
 __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(Params p, const float* __restrict__ pay,
                                                                                const float4* __restrict__ bounds,
                                                                                int* __restrict__ item_box) {
   extern __shared__ int tile[];  // SoA: 4 x TILE_NODES int32 channels (mv x, y, z, m)
-  constexpr int NTB = TILE_BRICKS * TILE_BRICKS * TILE_BRICKS;
-  __shared__ int touched[NTB];
   __shared__ int boxes[2][6];  // double-buffered by item parity: reset one while the other is live
   __shared__ float scale_s[4];
   const int nwork = *p.nwork;
   for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
-  const RotRows rr = make_rot_rows(p, pay, threadIdx.x & 3);
+  const int rot = threadIdx.x & 3;
+  const bool r1 = rot & 1, r2 = rot & 2;
+  int off[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) off[s] = ((s + rot) & 3) * TILE_NODES;
   int par = 0;
   for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, par ^= 1) {
     int* box = boxes[par];
@@ -557,52 +596,45 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
     const int by = (bin / p.nbin[2]) % p.nbin[1];
     const int bx = bin / (p.nbin[1] * p.nbin[2]);
     const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
-    // previous item's brick flags and box (its flush ended before the last barrier)
-    for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
+    // previous item's box (its flush ended before the last barrier)
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
     if (threadIdx.x < 4) {
       const float4 bd = bounds[wi];
-      const float bc[4] = {bd.x, bd.y, bd.z, bd.w};
-      scale_s[threadIdx.x] = channel_scale(bc[threadIdx.x], item.w);
+      const int c = threadIdx.x;
+      scale_s[c] = channel_scale(c == 0 ? bd.x : c == 1 ? bd.y : c == 2 ? bd.z : bd.w, item.w);
     }
     __syncthreads();
     const float S[4] = {scale_s[0], scale_s[1], scale_s[2], scale_s[3]};
     float sc[4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) sc[s] = rr.ch[s] == 0 ? S[0] : rr.ch[s] == 1 ? S[1] : rr.ch[s] == 2 ? S[2] : S[3];
+    for (int s = 0; s < 4; ++s) sc[s] = sel4(r1, r2, S[s & 3], S[(s + 1) & 3], S[(s + 2) & 3], S[(s + 3) & 3]);
     int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
-      int b[3], lc[3];
-      float f[3];
+      Payload q;
+      int lc[3];
       bool fits = true;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const float g = ldf(p, FX + a, i) * p.inv_dx;
         int bb = (int)floorf(g - 0.5f);
         bb = max(0, min(bb, p.res[a] - 3));
-        b[a] = bb;
-        f[a] = g - (float)bb;
+        q.b[a] = bb;
+        q.f[a] = g - (float)bb;
         lc[a] = bb - org[a];
         fits &= (lc[a] >= 0) && (lc[a] <= TILE - 3);
+        q.mv[a] = pay[a * p.cap + i];
       }
+#pragma unroll
+      for (int r = 0; r < 9; ++r) q.A[r] = pay[(3 + r) * p.cap + i];
+      q.m = pay[12 * p.cap + i];
       if (fits) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           lo_c[a] = min(lo_c[a], lc[a]);
           hi_c[a] = max(hi_c[a], lc[a]);
         }
-        p2g_scatter_rot(p, tile, org, rr, sc, i, b, f);
+        tile_scatter_rot(tile, off, r1, r2, sc, q, lc, p.dx);
       } else {
-        Payload q;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          q.b[a] = b[a];
-          q.f[a] = f[a];
-          q.mv[a] = pay[a * p.cap + i];
-        }
-#pragma unroll
-        for (int r = 0; r < 9; ++r) q.A[r] = pay[(3 + r) * p.cap + i];
-        q.m = pay[12 * p.cap + i];
         const float one[4] = {1.f, 1.f, 1.f, 1.f};
         p2g_scatter<false>(p, tile, org, q, one);
       }
@@ -624,34 +656,7 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
                                  : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
     }
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
-    // 2-D mapping: thread -> (ty, tz) column of the box, loop over tx
-    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
-      const int tz = z0 + (c & 15), ty = y0 + (c >> 4);
-      const int gj = org[1] + ty, gk = org[2] + tz;
-      if (tz > z1 || ty > y1 || x1 - 2 < x0 || gj < 0 || gk < 0 || gj >= p.res[1] || gk >= p.res[2]) continue;
-      const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
-                           ((gj & 3) << 2) + (gk & 3);
-      const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-      const int lby = (gj >> BRICK_SHIFT) - (org[1] >> BRICK_SHIFT);
-      const int lbz = (gk >> BRICK_SHIFT) - (org[2] >> BRICK_SHIFT);
-      for (int tx = x0; tx <= x1; ++tx) {
-        const int t = (tx * TILE + ty) * TILE + tz;
-        const int4 a = make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t],
-                                 tile[3 * TILE_NODES + t]);
-        if ((a.x | a.y | a.z | a.w) == 0) continue;
-        tile[t] = 0;
-        tile[TILE_NODES + t] = 0;
-        tile[2 * TILE_NODES + t] = 0;
-        tile[3 * TILE_NODES + t] = 0;
-        const int gi = org[0] + tx;
-        if (gi < 0 || gi >= p.res[0]) continue;
-        const long long idx = (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4);
-        atomicAdd(p.gm + idx, make_float4((float)a.x * inv[0], (float)a.y * inv[1],
-                                          (float)a.z * inv[2], (float)a.w * inv[3]));
-        const int lbx = (gi >> BRICK_SHIFT) - (org[0] >> BRICK_SHIFT);
-        if (atomicExch(&touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz], 1) == 0) mark_brick(p, idx);
-      }
-    }
+    flush_tile<2>(p, tile, org, x0, x1, y0, y1, z0, z1, inv);
     __syncthreads();
   }
 }
@@ -667,12 +672,6 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
 // into gm directly.  The item's exact new bounds (bounds_out, zeroed before
 // the launch) and node box are recorded for the next substep.
 constexpr float BOUND_SAFETY = 2.0f;
-
-__device__ __forceinline__ float sel4(bool r1, bool r2, float v0, float v1, float v2, float v3) {
-  const float a = r1 ? v1 : v0;
-  const float b = r1 ? v3 : v2;
-  return r2 ? b : a;
-}
 
 // Decode a work item: tile origin and the velocity-tile box (the base cells it
 // scattered from in the previous substep, item_box).
@@ -711,6 +710,18 @@ __device__ __forceinline__ void fused_item_prologue(const Params& p, const TileV
   }
 }
 
+#ifdef FUSED_PROFILE
+__device__ unsigned long long g_fprof[6];
+__device__ __forceinline__ long long fprof_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  return t;
+}
+#define FPROF_MARK(v) const long long v = fprof_clock()
+#else
+#define FPROF_MARK(v)
+#endif
+
 // Fused steady-state kernel, two barriers per item: [B] after the scatter
 // (tile complete) and [A] after the flush of this item overlapped with the
 // velocity-tile load of the CTA's next item (disjoint shared-memory regions).
@@ -720,8 +731,6 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   extern __shared__ float smem[];
   float* vtile = smem;                                           // 3 x TILE_NODES
   int* tile = reinterpret_cast<int*>(smem + 3 * TILE_NODES);     // 4 x TILE_NODES
-  constexpr int NTB = TILE_BRICKS * TILE_BRICKS * TILE_BRICKS;
-  __shared__ int touched[NTB];
   __shared__ int boxes[2][6];
   __shared__ float scale_s[2][4];
   const int nwork = *p.nwork;
@@ -741,6 +750,10 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     fused_item_prologue(p, tv0, vtile, it0, bounds_in[blockIdx.x], scale_s[0]);
   }
   __syncthreads();  // [A] first velocity tile + scales ready
+#ifdef FUSED_PROFILE
+  unsigned long long pr[5] = {0, 0, 0, 0, 0};
+  long long tA = fprof_clock();
+#endif
   for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, par ^= 1) {
     int* box = boxes[par];
     const int4 item = p.work[wi];
@@ -750,8 +763,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     const int* org = tv.org;
     const float4 bd = bounds_in[wi];
     const float B[4] = {bd.x * BOUND_SAFETY, bd.y * BOUND_SAFETY, bd.z * BOUND_SAFETY, bd.w};
-    // previous item's brick flags / box buffer (its flush ended before the last [A])
-    for (int t = threadIdx.x; t < NTB; t += blockDim.x) touched[t] = 0;
+    // previous item's box buffer (its flush ended before the last [A])
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
     const float S[4] = {scale_s[par][0], scale_s[par][1], scale_s[par][2], scale_s[par][3]};
     float sc[4];
@@ -789,46 +801,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
         lo_c[a] = min(lo_c[a], lc[a]);
         hi_c[a] = max(hi_c[a], lc[a]);
       }
-      // rotated, scaled channel rows (mass: b = m, A row = 0)
-      const float chb[4] = {q.mv[0], q.mv[1], q.mv[2], q.m};
-      float bs[4], as[4][3];
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        bs[s] = sel4(r1, r2, chb[s & 3], chb[(s + 1) & 3], chb[(s + 2) & 3], chb[(s + 3) & 3]) * sc[s];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const float ca[4] = {q.A[c], q.A[3 + c], q.A[6 + c], 0.0f};
-          as[s][c] = sel4(r1, r2, ca[s & 3], ca[(s + 1) & 3], ca[(s + 2) & 3], ca[(s + 3) & 3]) * sc[s];
-        }
-      }
-      float w[3][3], dxs[3][3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
-        w[a][0] = 0.5f * (t0 * t0);
-        w[a][1] = 0.75f - t1 * t1;
-        w[a][2] = 0.5f * (t2 * t2);
-#pragma unroll
-        for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * p.dx;
-      }
-      const int base = (lc[0] * TILE + lc[1]) * TILE + lc[2];
-#pragma unroll
-      for (int ii = 0; ii < 3; ++ii) {
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const float wij = w[0][ii] * w[1][j];
-          float bij[4];
-#pragma unroll
-          for (int s = 0; s < 4; ++s) bij[s] = bs[s] + as[s][0] * dxs[0][ii] + as[s][1] * dxs[1][j];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const float wt = wij * w[2][k];
-            int* t = tile + base + (ii * TILE + j) * TILE + k;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) atomicAdd(t + off[s], fixq(wt, bij[s] + as[s][2] * dxs[2][k]));
-          }
-        }
-      }
+      tile_scatter_rot(tile, off, r1, r2, sc, q, lc, p.dx);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -844,38 +817,16 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
         atomicMax(&box[3 + a], h);
       }
     }
+    FPROF_MARK(tb0);
     __syncthreads();  // [B] scatter complete; velocity tile free
+    FPROF_MARK(tb1);
     const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
     if (threadIdx.x == 0)
       item_box[wi] = x1 - 2 < x0 ? 0x00000FFF
                                  : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
-    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
-      const int tz = z0 + (c & 15), ty = y0 + (c >> 4);
-      const int gj = org[1] + ty, gk = org[2] + tz;
-      if (tz > z1 || ty > y1 || x1 - 2 < x0 || gj < 0 || gk < 0 || gj >= p.res[1] || gk >= p.res[2]) continue;
-      const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
-                           ((gj & 3) << 2) + (gk & 3);
-      const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-      const int lby = (gj >> BRICK_SHIFT) - (org[1] >> BRICK_SHIFT);
-      const int lbz = (gk >> BRICK_SHIFT) - (org[2] >> BRICK_SHIFT);
-      for (int tx = x0; tx <= x1; ++tx) {
-        const int t = (tx * TILE + ty) * TILE + tz;
-        const int4 a = make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t], tile[3 * TILE_NODES + t]);
-        if ((a.x | a.y | a.z | a.w) == 0) continue;
-        tile[t] = 0;
-        tile[TILE_NODES + t] = 0;
-        tile[2 * TILE_NODES + t] = 0;
-        tile[3 * TILE_NODES + t] = 0;
-        const int gi = org[0] + tx;
-        if (gi < 0 || gi >= p.res[0]) continue;
-        const long long idx = (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4);
-        atomicAdd(p.gm + idx, make_float4((float)a.x * inv[0], (float)a.y * inv[1], (float)a.z * inv[2],
-                                          (float)a.w * inv[3]));
-        const int lbx = (gi >> BRICK_SHIFT) - (org[0] >> BRICK_SHIFT);
-        if (atomicExch(&touched[(lbx * TILE_BRICKS + lby) * TILE_BRICKS + lbz], 1) == 0) mark_brick(p, idx);
-      }
-    }
+    flush_tile<4>(p, tile, org, x0, x1, y0, y1, z0, z1, inv);
+    FPROF_MARK(tf);
     // overlapped with the flush: the CTA's next item's velocity tile + scales
     const int nxt = wi + gridDim.x;
     if (nxt < nwork) {
@@ -884,8 +835,21 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
       fused_item_geometry(p, itn, item_box[nxt], tn);
       fused_item_prologue(p, tn, vtile, itn, bounds_in[nxt], scale_s[par ^ 1]);
     }
+    FPROF_MARK(ta0);
     __syncthreads();  // [A] flush complete (tile zero), next velocity tile ready
+#ifdef FUSED_PROFILE
+    {
+      const long long ta1 = fprof_clock();
+      pr[0] += tb0 - tA; pr[1] += tb1 - tb0; pr[2] += tf - tb1; pr[3] += ta0 - tf; pr[4] += ta1 - ta0;
+      tA = ta1;
+    }
+#endif
   }
+#ifdef FUSED_PROFILE
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 5; ++k) atomicAdd(&g_fprof[k], pr[k]);
+  if (threadIdx.x == 0) atomicAdd(&g_fprof[5], 1ull);
+#endif
   warp_count_add(p.inverted, inverted);
 }
 

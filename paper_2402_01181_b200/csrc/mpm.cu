@@ -666,6 +666,15 @@ int mpm_destroy(mpm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+#ifdef FUSED_PROFILE
+  {
+    unsigned long long h[6];
+    cudaMemcpyFromSymbol(h, g_fprof, sizeof(h));
+    const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
+    fprintf(stderr, "[fused profile] warp-cycles: particles %.3f  wait[B] %.3f  flush %.3f  next-tile %.3f  wait[A] %.3f  (total %.3e, ctas %llu)\n",
+            h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, tot, h[5]);
+  }
+#endif
   invalidate_graphs(ctx);
   void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box, ctx->mflag, ctx->mig_rows[0], ctx->mig_rows[1], ctx->h_send_ids[0], ctx->h_send_ids[1],
                   ctx->h_send_data[0], ctx->h_send_data[1], ctx->h_recv_ids[0], ctx->h_recv_ids[1], ctx->h_recv_data[0],
