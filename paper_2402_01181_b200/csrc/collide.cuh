@@ -163,6 +163,47 @@ __device__ __forceinline__ bool collider_near(const Colliders& cs, int ci, float
   return true;
 }
 
+// The same test with the fp32 pose and the inflated box precomputed once per
+// CTA: local p in [lo, hi] per axis (non-strict: at least as conservative).
+struct ColliderNearF {
+  float R[9], T[3];
+  float lo[3], hi[3];
+  __device__ __forceinline__ bool near(float x, float y, float z) const {
+    const float d0 = x - T[0], d1 = y - T[1], d2 = z - T[2];
+    const float px = R[0] * d0 + R[3] * d1 + R[6] * d2;
+    const float py = R[1] * d0 + R[4] * d1 + R[7] * d2;
+    const float pz = R[2] * d0 + R[5] * d1 + R[8] * d2;
+    return px >= lo[0] && px <= hi[0] && py >= lo[1] && py <= hi[1] && pz >= lo[2] && pz <= hi[2];
+  }
+};
+
+__device__ inline ColliderNearF make_near_f(const Colliders& cs, int ci, float theta_m) {
+  const ColliderGeo& g = cs.geo[ci];
+  const ColliderPose& q = cs.pose[ci];
+  ColliderNearF f;
+  for (int k = 0; k < 9; ++k) f.R[k] = (float)q.R[k];
+  for (int k = 0; k < 3; ++k) f.T[k] = (float)q.T[k];
+  if (g.kind == 0) {
+    for (int k = 0; k < 3; ++k) {
+      f.hi[k] = (float)g.half[k] + theta_m;
+      f.lo[k] = -f.hi[k];
+    }
+  } else if (g.far_min >= theta_m) {
+    const float m = 1e-4f * (float)g.sdf_ext + 1e-6f;
+    const float e = (float)g.sdf_ext + 2.0f * m;
+    for (int k = 0; k < 3; ++k) {
+      f.lo[k] = (float)g.sdf_bmin[k] - m;
+      f.hi[k] = f.lo[k] + e;
+    }
+  } else {
+    for (int k = 0; k < 3; ++k) {
+      f.lo[k] = -INFINITY;
+      f.hi[k] = INFINITY;
+    }
+  }
+  return f;
+}
+
 // Merged field at one node: min distance, ties to the lowest index, id -1
 // beyond cap = 2 theta (kernels.py:180-191).
 __device__ inline int nearest_collider(const Colliders& cs, double wx, double wy, double wz,

@@ -39,6 +39,10 @@ constexpr int FUSED_K_THREADS = MPM_FUSED_THREADS;  // fused steady-state kernel
 constexpr int FUSED_MIN_BLOCKS = MPM_FUSED_MINB;
 constexpr int P2G_THREADS = 256;        // stage B (p2g_tile_kernel)
 constexpr int P2G_MIN_BLOCKS = 3;
+#ifndef MPM_GRIDOP_MINB
+#define MPM_GRIDOP_MINB 2
+#endif
+constexpr int GRIDOP_MIN_BLOCKS = MPM_GRIDOP_MINB;
 constexpr int NPAY = 13;                // payload floats per particle: m v (3), A (9), m
 constexpr int CHUNK = 4096;               // max particles per work item (larger bins split evenly)
 constexpr int MIN_CHUNK = 256;            // small scenes: items shrink to this so every SM gets work

@@ -377,6 +377,27 @@ __device__ __forceinline__ void load_vtile_column(const Params& p, float* vtile,
   }
 }
 
+// Same column with LDGSTS (cp.async, 4-byte, L1-allocating): no registers and
+// no stall at issue; completion is awaited (cp.async.wait_all) before the
+// barrier that publishes the tile.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void load_vtile_column_async(const Params& p, float* vtile, int orgx, int x0, int x1,
+                                                        int ty, int tz, long long yz, long long xstride) {
+  for (int tx = x0; tx <= x1; ++tx) {
+    const int gi = orgx + tx;
+    const float* src = reinterpret_cast<const float*>(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
+    const int t = (tx * TILE + ty) * TILE + tz;
+    cp_async4(vtile + t, src);
+    cp_async4(vtile + TILE_NODES + t, src + 1);
+    cp_async4(vtile + 2 * TILE_NODES + t, src + 2);
+  }
+}
+
 // Stage A of a substep: G2P(n) -> advect -> F update -> Neo-Hookean stress for
 // every particle of a work item; writes x, F and the P2G payload (m v, A, m:
 // NPAY floats SoA) and the item's exact per-channel bound (warp max ->
@@ -690,23 +711,28 @@ __device__ __forceinline__ void fused_item_geometry(const Params& p, const int4 
   }
 }
 
-// Fill the velocity tile of an item and its channel scales (called by the
-// whole CTA in the phase before the item's scatter).
-__device__ __forceinline__ void fused_item_prologue(const Params& p, const TileVel& tv, float* vtile, const int4 item,
-                                                    const float4 bd, float* scale_slot) {
+// Start the (asynchronous) fill of an item's velocity tile; the caller waits
+// with cp_async_wait_all before the barrier that publishes it.
+__device__ __forceinline__ void fused_item_vtile_issue(const Params& p, const TileVel& tv, float* vtile) {
+  if (tv.lo[0] > tv.hi[0]) return;
+  const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
   for (int c = threadIdx.x; c < 256; c += blockDim.x) {
     const int ty = tv.lo[1] + (c >> 4), tz = tv.lo[2] + (c & 15);
     const int gj = tv.org[1] + ty, gk = tv.org[2] + tz;
-    if (tv.lo[0] <= tv.hi[0] && ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
+    if (ty <= tv.hi[1] + 2 && tz <= tv.hi[2] + 2 && gj < p.res[1] && gk < p.res[2]) {
       const long long yz = ((long long)(gj >> BRICK_SHIFT) * p.nb[2] + (gk >> BRICK_SHIFT)) * 64 +
                            ((gj & 3) << 2) + (gk & 3);
-      const long long xstride = (long long)p.nb[1] * p.nb[2] * 64;
-      load_vtile_column(p, vtile, tv.org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
+      load_vtile_column_async(p, vtile, tv.org[0], tv.lo[0], tv.hi[0] + 2, ty, tz, yz, xstride);
     }
   }
+}
+
+// An item's channel scales (threads 0..3).
+__device__ __forceinline__ void fused_item_scales(const int4 item, const float4 bd, float* scale_slot) {
   if (threadIdx.x < 4) {
-    const float b[4] = {bd.x * BOUND_SAFETY, bd.y * BOUND_SAFETY, bd.z * BOUND_SAFETY, bd.w};
-    scale_slot[threadIdx.x] = channel_scale(b[threadIdx.x], item.w);
+    const int c = threadIdx.x;
+    const float b = c == 0 ? bd.x * BOUND_SAFETY : c == 1 ? bd.y * BOUND_SAFETY : c == 2 ? bd.z * BOUND_SAFETY : bd.w;
+    scale_slot[c] = channel_scale(b, item.w);
   }
 }
 
@@ -717,9 +743,15 @@ __device__ __forceinline__ long long fprof_clock() {
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
   return t;
 }
+__device__ __forceinline__ long long fprof_clock_dep(int dep) {
+  if (dep == 0x7fffffff) __trap();  // the branch waits for dep (a shared load behind the barrier)
+  return fprof_clock();
+}
 #define FPROF_MARK(v) const long long v = fprof_clock()
+#define FPROF_MARK_DEP(v, d) const long long v = fprof_clock_dep(d)
 #else
 #define FPROF_MARK(v)
+#define FPROF_MARK_DEP(v, d)
 #endif
 
 // Fused steady-state kernel, two barriers per item: [B] after the scatter
@@ -733,6 +765,9 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   int* tile = reinterpret_cast<int*>(smem + 3 * TILE_NODES);     // 4 x TILE_NODES
   __shared__ int boxes[2][6];
   __shared__ float scale_s[2][4];
+  __shared__ int4 nxt_item;
+  __shared__ int nxt_box;
+  __shared__ float4 nxt_bounds;
   const int nwork = *p.nwork;
   for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
@@ -747,7 +782,9 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     TileVel tv0;
     const int4 it0 = p.work[blockIdx.x];
     fused_item_geometry(p, it0, item_box[blockIdx.x], tv0);
-    fused_item_prologue(p, tv0, vtile, it0, bounds_in[blockIdx.x], scale_s[0]);
+    fused_item_vtile_issue(p, tv0, vtile);
+    fused_item_scales(it0, bounds_in[blockIdx.x], scale_s[0]);
+    cp_async_wait_all();
   }
   __syncthreads();  // [A] first velocity tile + scales ready
 #ifdef FUSED_PROFILE
@@ -760,6 +797,12 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     TileVel tv;
     tv.t = vtile;
     fused_item_geometry(p, item, item_box[wi], tv);
+    if (threadIdx.x == 32 && wi + gridDim.x < nwork) {  // next item's descriptor, read after [B]
+      const int nxt = wi + gridDim.x;
+      nxt_item = p.work[nxt];
+      nxt_box = item_box[nxt];
+      nxt_bounds = bounds_in[nxt];
+    }
     const int* org = tv.org;
     const float4 bd = bounds_in[wi];
     const float B[4] = {bd.x * BOUND_SAFETY, bd.y * BOUND_SAFETY, bd.z * BOUND_SAFETY, bd.w};
@@ -819,27 +862,31 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     }
     FPROF_MARK(tb0);
     __syncthreads();  // [B] scatter complete; velocity tile free
-    FPROF_MARK(tb1);
+    FPROF_MARK_DEP(tb1, *(volatile int*)&boxes[par][0]);
     const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
     if (threadIdx.x == 0)
       item_box[wi] = x1 - 2 < x0 ? 0x00000FFF
                                  : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
+    // the CTA's next item: velocity-tile copies issued before the flush so
+    // their L2 latency hides under it
+    const bool has_next = wi + gridDim.x < nwork;
+    int4 itn;
+    if (has_next) {
+      TileVel tn;
+      itn = nxt_item;
+      fused_item_geometry(p, itn, nxt_box, tn);
+      fused_item_vtile_issue(p, tn, vtile);
+    }
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
     flush_tile<4>(p, tile, org, x0, x1, y0, y1, z0, z1, inv);
     FPROF_MARK(tf);
-    // overlapped with the flush: the CTA's next item's velocity tile + scales
-    const int nxt = wi + gridDim.x;
-    if (nxt < nwork) {
-      TileVel tn;
-      const int4 itn = p.work[nxt];
-      fused_item_geometry(p, itn, item_box[nxt], tn);
-      fused_item_prologue(p, tn, vtile, itn, bounds_in[nxt], scale_s[par ^ 1]);
-    }
+    if (has_next) fused_item_scales(itn, nxt_bounds, scale_s[par ^ 1]);
+    cp_async_wait_all();
     FPROF_MARK(ta0);
     __syncthreads();  // [A] flush complete (tile zero), next velocity tile ready
 #ifdef FUSED_PROFILE
     {
-      const long long ta1 = fprof_clock();
+      const long long ta1 = fprof_clock_dep(*(volatile int*)&scale_s[par ^ 1][0]);
       pr[0] += tb0 - tA; pr[1] += tb1 - tb0; pr[2] += tf - tb1; pr[3] += ta0 - tf; pr[4] += ta1 - ta0;
       tA = ta1;
     }
@@ -870,6 +917,22 @@ __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
   for (int q = 0; q < 9; ++q) stf(p, FC + q, i, C[q]);
 }
 
+// Exact fp64 field + contact response at one massive node inside the fp32
+// prefilter band.  Out of line: only a few percent of the nodes get here, and
+// keeping its fp64 register footprint out of grid_op_kernel lets 4 CTAs of
+// the streaming path reside per SM.
+__device__ __noinline__ float3 grid_contact(const Colliders cs, double cap, double wx, double wy, double wz, float v0,
+                                            float v1, float v2) {
+  double best;
+  const int ci = nearest_collider(cs, wx, wy, wz, cap, best);
+  if (best < cs.theta && ci >= 0) {
+    double vv[3] = {v0, v1, v2};
+    resolve_contact(cs, ci, wx, wy, wz, vv);
+    return make_float3((float)vv[0], (float)vv[1], (float)vv[2]);
+  }
+  return make_float3(v0, v1, v2);
+}
+
 // Grid op (kernels.py:347-436) over active bricks (or all bricks when DENSE):
 // one warp per 4^3 brick, two nodes per lane (both loads in flight).
 // Zero-mass nodes pass momentum through unchanged (kernels.py:364-365).
@@ -878,16 +941,22 @@ __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
 // (collide.cuh: collider_far) is below theta + margin -- nodes the bound
 // clears cannot be in contact, so results are unchanged.  When `clear`, gm
 // is zeroed for the next P2G.
-__device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs_all, double cap, float4 a, int gi,
-                                            int gj, int gk) {
+__device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs_all, const ColliderNearF* nf,
+                                            bool single_env, double cap, float4 a, int gi, int gj, int gk) {
   if (!(a.w > 0.0f) || gi >= p.res[0] || gj >= p.res[1] || gk >= p.res[2]) return a;
   // global node coordinates (slab window offset), environment tile, tile-local coordinates
   gi += p.goff[0];
   gj += p.goff[1];
   gk += p.goff[2];
-  const int ei = gi / p.env_res[0], ej = gj / p.env_res[1], ek = gk / p.env_res[2];
-  const Colliders cs = env_colliders(cs_all, ei, ej, ek);
-  const int li = gi - ei * p.env_res[0], lj = gj - ej * p.env_res[1], lk = gk - ek * p.env_res[2];
+  int li = gi, lj = gj, lk = gk;
+  Colliders cs = cs_all;
+  if (!single_env) {
+    const int ei = gi / p.env_res[0], ej = gj / p.env_res[1], ek = gk / p.env_res[2];
+    cs = env_colliders(cs_all, ei, ej, ek);
+    li = gi - ei * p.env_res[0];
+    lj = gj - ej * p.env_res[1];
+    lk = gk - ek * p.env_res[2];
+  }
   const float inv_m = 1.0f / a.w;
   float v0 = a.x * inv_m + p.dt * p.gravity[0];
   float v1 = a.y * inv_m + p.dt * p.gravity[1];
@@ -895,18 +964,16 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
   if (cs.theta >= 0.0 && cs.count > 0) {
     const float fx = (float)gi * p.dx, fy = (float)gj * p.dx, fz = (float)gk * p.dx;
     bool near = false;
-    for (int ci = 0; ci < cs.count; ++ci) near |= collider_near(cs, ci, fx, fy, fz, cs.theta_f);
+    if (nf) {
+      for (int ci = 0; ci < cs.count; ++ci) near |= nf[ci].near(fx, fy, fz);
+    } else {
+      for (int ci = 0; ci < cs.count; ++ci) near |= collider_near(cs, ci, fx, fy, fz, cs.theta_f);
+    }
     if (near) {
-      const double wx = (double)gi * p.dx64, wy = (double)gj * p.dx64, wz = (double)gk * p.dx64;
-      double best;
-      const int ci = nearest_collider(cs, wx, wy, wz, cap, best);
-      if (best < cs.theta && ci >= 0) {
-        double vv[3] = {v0, v1, v2};
-        resolve_contact(cs, ci, wx, wy, wz, vv);
-        v0 = (float)vv[0];
-        v1 = (float)vv[1];
-        v2 = (float)vv[2];
-      }
+      const float3 v = grid_contact(cs, cap, (double)gi * p.dx64, (double)gj * p.dx64, (double)gk * p.dx64, v0, v1, v2);
+      v0 = v.x;
+      v1 = v.y;
+      v2 = v.z;
     }
   }
   const int bw = p.bwidth;
@@ -925,21 +992,40 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
 }
 
 template <bool DENSE>
-__global__ void __launch_bounds__(256) grid_op_kernel(Params p, Colliders cs, int clear) {
+__global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params p, Colliders cs, int clear) {
+  // one table for the whole grid: the fp32 prefilter boxes are staged in
+  // shared memory once per CTA (per-environment tables use collider_near)
+  __shared__ ColliderNearF nf_s[MAX_COLLIDERS];
+  const bool staged = !cs.per_env && cs.theta >= 0.0 && cs.count > 0 && cs.count <= MAX_COLLIDERS;
+  if (staged && threadIdx.x < cs.count) nf_s[threadIdx.x] = make_near_f(cs, threadIdx.x, cs.theta_f);
+  __syncthreads();
+  const ColliderNearF* nf = staged ? nf_s : nullptr;
+  const bool single_env = p.env_res[0] == p.gres[0] && p.env_res[1] == p.gres[1] && p.env_res[2] == p.gres[2];
   const long long nitems = DENSE ? (long long)p.nb[0] * p.nb[1] * p.nb[2] : (long long)*p.active_count;
   const int lane = threadIdx.x & 31;
   const double cap = 2.0 * cs.theta;
-  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems;
-       it += (long long)gridDim.x * (blockDim.x >> 5)) {
-    const long long b = DENSE ? it : (long long)p.active_list[it];
+  const long long stride = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
+  long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (it >= nitems) return;
+  // one brick per warp iteration (lane -> nodes lane, lane + 32); the next
+  // brick's momentum is loaded before this one is processed
+  long long b = DENSE ? it : (long long)p.active_list[it];
+  float4 a0 = p.gm[(b << 6) | lane], a1 = p.gm[((b << 6) | lane) + 32];
+  for (; it < nitems; it += stride) {
+    const long long nit = it + stride;
+    long long nb = b;
+    float4 n0 = a0, n1 = a1;
+    if (nit < nitems) {
+      nb = DENSE ? nit : (long long)p.active_list[nit];
+      n0 = p.gm[(nb << 6) | lane];
+      n1 = p.gm[((nb << 6) | lane) + 32];
+    }
     const int b32 = (int)b;
     const int bk = b32 % p.nb[2], bj = (b32 / p.nb[2]) % p.nb[1], bi = b32 / (p.nb[2] * p.nb[1]);
-    const long long i0 = (b << 6) | lane, i1 = i0 + 32;  // local nodes lane, lane + 32
-    const float4 a0 = p.gm[i0];
-    const float4 a1 = p.gm[i1];
-    const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
-    const float4 o0 = grid_node(p, cs, cap, a0, bi * 4 + li0, bj * 4 + lj, bk * 4 + lk);
-    const float4 o1 = grid_node(p, cs, cap, a1, bi * 4 + li0 + 2, bj * 4 + lj, bk * 4 + lk);
+    const long long i0 = (b << 6) | lane, i1 = i0 + 32;
+    const float4 o0 = grid_node(p, cs, nf, single_env, cap, a0, bi * 4 + li0, bj * 4 + lj, bk * 4 + lk);
+    const float4 o1 = grid_node(p, cs, nf, single_env, cap, a1, bi * 4 + li0 + 2, bj * 4 + lj, bk * 4 + lk);
     p.gv[i0] = o0;
     p.gv[i1] = o1;
     if (clear) {
@@ -947,6 +1033,9 @@ __global__ void __launch_bounds__(256) grid_op_kernel(Params p, Colliders cs, in
       p.gm[i1] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (lane == 0) p.brick_flag[b] = 0;
+    b = nb;
+    a0 = n0;
+    a1 = n1;
   }
 }
 

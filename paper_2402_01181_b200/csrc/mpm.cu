@@ -647,7 +647,10 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, dyn);
       return ctx->sms * std::max(1, o);
     };
-    ctx->gridop_blocks = ctx->sms * 8;  // measured: more, shorter CTAs beat a persistent grid here
+    {
+      const char* gb = getenv("SOFTMPM_GRIDOP_BLOCKS");  // CTAs per SM (A/B runs)
+      ctx->gridop_blocks = ctx->sms * (gb && atoi(gb) > 0 ? atoi(gb) : GRIDOP_MIN_BLOCKS);
+    }
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
     ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
