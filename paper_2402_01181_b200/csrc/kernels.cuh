@@ -18,6 +18,14 @@
 
 namespace mpm {
 
+#ifdef FUSED_PROFILE
+__device__ unsigned long long g_fprof[6];
+__device__ unsigned long long g_fcnt[4];  // particles, G2P off-tile, P2G fallback
+#define FPROF_COUNT(k) atomicAdd(&g_fcnt[k], 1ull)
+#else
+#define FPROF_COUNT(k)
+#endif
+
 __device__ __forceinline__ void mark_brick(const Params& p, long long idx) {
   int b = (int)(idx >> 6);
   if (*((volatile int*)p.brick_flag + b) == 0) {
@@ -26,6 +34,23 @@ __device__ __forceinline__ void mark_brick(const Params& p, long long idx) {
       p.active_list[s] = b;
     }
   }
+}
+
+// Mark the (up to 2x2x2) bricks of a 3^3 stencil with base cell b: all flag
+// loads are issued before any is tested (one L2 round trip, not one per node).
+__device__ __forceinline__ void mark_stencil_bricks(const Params& p, const int b[3]) {
+  const int bx0 = b[0] >> BRICK_SHIFT, by0 = b[1] >> BRICK_SHIFT, bz0 = b[2] >> BRICK_SHIFT;
+  const int dx = ((b[0] + 2) >> BRICK_SHIFT) - bx0, dy = ((b[1] + 2) >> BRICK_SHIFT) - by0,
+            dz = ((b[2] + 2) >> BRICK_SHIFT) - bz0;
+  int id[8], f[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    id[k] = ((bx0 + ((k >> 2) & dx)) * p.nb[1] + by0 + ((k >> 1) & dy)) * p.nb[2] + bz0 + (k & dz);
+    f[k] = *((volatile int*)p.brick_flag + id[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (f[k] == 0 && atomicExch(&p.brick_flag[id[k]], 1) == 0) p.active_list[atomicAdd(p.active_count, 1)] = id[k];
 }
 
 __device__ __forceinline__ void warp_count_add(unsigned long long* dst, unsigned v) {
@@ -244,13 +269,12 @@ __device__ __forceinline__ void p2g_scatter(const Params& p, int* tile, const in
         } else {
           atomicAdd(p.gm + idx, make_float4(wt * (bij[0] + az[k][0]), wt * (bij[1] + az[k][1]),
                                             wt * (bij[2] + az[k][2]), wt * ms));
-          mark_brick(p, idx);
         }
       }
     }
   }
+  if (!TILE_MODE) mark_stencil_bricks(p, q.b);
 }
-
 
 // Raw particle fields of one slot.
 template <bool G2P>
@@ -295,10 +319,12 @@ __device__ __forceinline__ float compute_payload(const Params& p, long long i, P
       stencil(r.x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
       if (tv) in_tile &= (b[a] - tv->org[a] >= tv->lo[a]) && (b[a] - tv->org[a] <= tv->hi[a]);
     }
-    if (in_tile)
+    if (in_tile) {
       g2p_gather(p, *tv, b, f, w, v, C);
-    else
+    } else {
+      if (tv) FPROF_COUNT(1);
       g2p_gather(p, global_vel(p), b, f, w, v, C);
+    }
     advect(p, r.x, v);
     if (STORE) {
 #pragma unroll
@@ -737,7 +763,6 @@ __device__ __forceinline__ void fused_item_scales(const int4 item, const float4 
 }
 
 #ifdef FUSED_PROFILE
-__device__ unsigned long long g_fprof[6];
 __device__ __forceinline__ long long fprof_clock() {
   long long t;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
@@ -828,13 +853,21 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
         mx[c] = fmaxf(mx[c], bnd[c]);
         fits &= bnd[c] <= B[c];
       }
+#ifdef FUSED_PROFILE
+      const bool bound_ok = fits;
+#endif
       int lc[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         lc[a] = q.b[a] - org[a];
         fits &= (lc[a] >= 0) && (lc[a] <= TILE - 3);
       }
+      FPROF_COUNT(0);
       if (!fits) {
+        FPROF_COUNT(2);
+#ifdef FUSED_PROFILE
+        if (!bound_ok) FPROF_COUNT(3);
+#endif
         const float one[4] = {1.f, 1.f, 1.f, 1.f};
         p2g_scatter<false>(p, tile, org, q, one);
         continue;

@@ -487,7 +487,7 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   {
     TimedRegion tr(ctx, 5);
     fused_kernel<<<ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
-        p, ctx->item_bounds, ctx->item_bounds2, ctx->item_box);
+          p, ctx->item_bounds, ctx->item_bounds2, ctx->item_box);
     LAUNCHED();
   }
   std::swap(ctx->item_bounds, ctx->item_bounds2);
@@ -676,6 +676,10 @@ int mpm_destroy(mpm_ctx* ctx) {
     const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
     fprintf(stderr, "[fused profile] warp-cycles: particles %.3f  wait[B] %.3f  flush %.3f  next-tile %.3f  wait[A] %.3f  (total %.3e, ctas %llu)\n",
             h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, tot, h[5]);
+    unsigned long long c[4];
+    cudaMemcpyFromSymbol(c, g_fcnt, sizeof(c));
+    fprintf(stderr, "[fused profile] particles %llu  g2p off-tile %llu (%.4f)  p2g fallback %llu (%.4f, bound %llu)\n",
+            c[0], c[1], c[1] / (double)(c[0] ? c[0] : 1), c[2], c[2] / (double)(c[0] ? c[0] : 1), c[3]);
   }
 #endif
   invalidate_graphs(ctx);
