@@ -90,6 +90,7 @@ struct Params {
   // work items (bin, start, end, 0)
   const int4* work;
   const int* nwork;
+  int* work_next;    // dynamic work-item counter (zeroed per launch)
 };
 
 __host__ __device__ inline long long node_index(int i, int j, int k, int nby, int nbz) {

@@ -793,6 +793,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   __shared__ int4 nxt_item;
   __shared__ int nxt_box;
   __shared__ float4 nxt_bounds;
+  __shared__ int nxt_wi;
   const int nwork = *p.nwork;
   for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
@@ -803,6 +804,8 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   for (int s = 0; s < 4; ++s) off[s] = ((s + rot) & 3) * TILE_NODES;
   unsigned inverted = 0;
   int par = 0;
+  // dynamic scheduling over the size-sorted work list: the first gridDim.x
+  // items are taken in launch order, later ones from the counter
   if (blockIdx.x < nwork) {
     TileVel tv0;
     const int4 it0 = p.work[blockIdx.x];
@@ -816,17 +819,20 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   unsigned long long pr[5] = {0, 0, 0, 0, 0};
   long long tA = fprof_clock();
 #endif
-  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x, par ^= 1) {
+  for (int wi = blockIdx.x; wi < nwork; par ^= 1) {
     int* box = boxes[par];
     const int4 item = p.work[wi];
     TileVel tv;
     tv.t = vtile;
     fused_item_geometry(p, item, item_box[wi], tv);
-    if (threadIdx.x == 32 && wi + gridDim.x < nwork) {  // next item's descriptor, read after [B]
-      const int nxt = wi + gridDim.x;
-      nxt_item = p.work[nxt];
-      nxt_box = item_box[nxt];
-      nxt_bounds = bounds_in[nxt];
+    if (threadIdx.x == 32) {  // next item (claimed now) and its descriptor, read after [B]
+      const int nxt = gridDim.x + atomicAdd(p.work_next, 1);
+      nxt_wi = nxt;
+      if (nxt < nwork) {
+        nxt_item = p.work[nxt];
+        nxt_box = item_box[nxt];
+        nxt_bounds = bounds_in[nxt];
+      }
     }
     const int* org = tv.org;
     const float4 bd = bounds_in[wi];
@@ -902,7 +908,8 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
                                  : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
     // the CTA's next item: velocity-tile copies issued before the flush so
     // their L2 latency hides under it
-    const bool has_next = wi + gridDim.x < nwork;
+    const int wnext = nxt_wi;
+    const bool has_next = wnext < nwork;
     int4 itn;
     if (has_next) {
       TileVel tn;
@@ -917,6 +924,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     cp_async_wait_all();
     FPROF_MARK(ta0);
     __syncthreads();  // [A] flush complete (tile zero), next velocity tile ready
+    wi = wnext;
 #ifdef FUSED_PROFILE
     {
       const long long ta1 = fprof_clock_dep(*(volatile int*)&scale_s[par ^ 1][0]);
@@ -1189,18 +1197,56 @@ __global__ void gather_permute_kernel(const float* __restrict__ src, const int* 
   dst_orig[d] = __ldg(src_orig + s);
 }
 
-__global__ void make_work_kernel(const int* bin_count, const int* bin_start, const int* bin_maxcnt, int nbins,
-                                 int4* work, int* nwork, int chunk) {
+// Work list, sorted by decreasing size class (whole CTA rounds of
+// FUSED_K_THREADS particles) so that the dynamically scheduled kernels hand
+// out the large items first (longest-processing-time order) and finish on
+// the small ones.  Three launches: count per class, class offsets, emit.
+constexpr int WORK_CLASSES = CHUNK / 256 + 2;
+
+__device__ __forceinline__ int work_items_of(int c, int chunk, int& per) {
+  const int items = (c + chunk - 1) / chunk;
+  per = (c + items - 1) / items;  // equal splits (no tiny tail item)
+  return items;
+}
+
+__device__ __forceinline__ int work_class(int size) {
+  return min((size + FUSED_K_THREADS - 1) / FUSED_K_THREADS, WORK_CLASSES - 1);
+}
+
+__global__ void make_work_count_kernel(const int* bin_count, int nbins, int chunk, int* class_count) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nbins) return;
   const int c = bin_count[b];
   if (!c) return;
-  const int items = (c + chunk - 1) / chunk;
-  const int per = (c + items - 1) / items;  // equal splits (no tiny tail item)
-  const int base = atomicAdd(nwork, items);
+  int per;
+  const int items = work_items_of(c, chunk, per);
+  for (int t = 0; t < items; ++t) atomicAdd(&class_count[work_class(min(per, c - t * per))], 1);
+}
+
+__global__ void make_work_offsets_kernel(const int* class_count, int* class_cursor, int* nwork) {
+  if (threadIdx.x != 0) return;
+  int s = 0;
+  for (int k = WORK_CLASSES - 1; k >= 0; --k) {
+    class_cursor[k] = s;
+    s += class_count[k];
+  }
+  *nwork = s;
+}
+
+__global__ void make_work_kernel(const int* bin_count, const int* bin_start, const int* bin_maxcnt, int nbins,
+                                 int4* work, int* class_cursor, int chunk) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbins) return;
+  const int c = bin_count[b];
+  if (!c) return;
+  int per;
+  const int items = work_items_of(c, chunk, per);
   const int s = bin_start[b];
-  for (int t = 0; t < items; ++t)
-    work[base + t] = make_int4(b, s + t * per, min(s + (t + 1) * per, s + c), bin_maxcnt[b]);
+  for (int t = 0; t < items; ++t) {
+    const int size = min(per, c - t * per);
+    const int pos = atomicAdd(&class_cursor[work_class(size)], 1);
+    work[pos] = make_int4(b, s + t * per, s + t * per + size, bin_maxcnt[b]);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -34,7 +34,7 @@ struct mpm_ctx {
   float4* gv = nullptr;
   int* brick_flag = nullptr;
   int* active_list = nullptr;
-  int* counters = nullptr;  // [0] active_count, [1] nwork
+  int* counters = nullptr;  // [0] active_count, [1] nwork, [2] halo, [3] work_next, [4..] work classes
   int grid_phase = 0;       // 0 momentum view, 1 velocity view, 2 uploaded velocities
   int grid_dirty = 2;       // 0 clean, 1 active-list bricks dirty, 2 fully dirty
 
@@ -134,7 +134,7 @@ struct mpm_ctx {
   std::vector<cudaEvent_t> event_pool;
   double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
-  int items_per_sm = 8;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
+  int items_per_sm = 4;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
 };
 
 namespace {
@@ -301,6 +301,7 @@ Params make_params(mpm_ctx* ctx) {
   p.inverted = ctx->inverted;
   p.work = ctx->work;
   p.nwork = ctx->counters + 1;
+  p.work_next = ctx->counters + 3;
   return p;
 }
 
@@ -450,8 +451,16 @@ int rebin(mpm_ctx* ctx) {
   ctx->cur = nxt;
   // ~4 items per SM at least: small scenes split bins, large ones keep whole bins
   const int chunk = (int)std::max<long long>(MIN_CHUNK, std::min<long long>(CHUNK, ctx->n / ((long long)ctx->items_per_sm * ctx->sms)));
+  static_assert(4 + 2 * WORK_CLASSES <= 64, "counters too small");
+  int* classes = ctx->counters + 4;
+  CK(cudaMemsetAsync(classes, 0, sizeof(int) * WORK_CLASSES, ctx->stream));
+  make_work_count_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(ctx->bin_count, ctx->nbins, chunk,
+                                                                               classes);
+  LAUNCHED();
+  make_work_offsets_kernel<<<1, 32, 0, ctx->stream>>>(classes, classes + WORK_CLASSES, ctx->counters + 1);
+  LAUNCHED();
   make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(
-      ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, ctx->counters + 1, chunk);
+      ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, classes + WORK_CLASSES, chunk);
   LAUNCHED();
   return 0;
 }
@@ -484,6 +493,7 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   }
   // fused: bounds_in = item_bounds (last substep), bounds_out = item_bounds2, then swap
   CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
+  CK(cudaMemsetAsync(ctx->counters + 3, 0, sizeof(int), ctx->stream));
   {
     TimedRegion tr(ctx, 5);
     fused_kernel<<<ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
@@ -617,11 +627,11 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
   int rc = 0;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc) rc = alloc_grid(ctx);
-  if (!rc) rc = dalloc(ctx, &ctx->counters, 8);
+  if (!rc) rc = dalloc(ctx, &ctx->counters, 64);
   if (!rc) rc = dalloc(ctx, &ctx->inverted, 1);
   if (!rc) rc = dalloc(ctx, &ctx->flag, 1);
   if (!rc) rc = ensure_scan(ctx, ctx->nbins);
-  if (!rc && cudaMemsetAsync(ctx->counters, 0, 32, ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc && cudaMemsetAsync(ctx->counters, 0, 64 * sizeof(int), ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
