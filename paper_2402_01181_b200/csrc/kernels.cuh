@@ -782,7 +782,7 @@ __device__ __forceinline__ long long fprof_clock_dep(int dep) {
 // Fused steady-state kernel, two barriers per item: [B] after the scatter
 // (tile complete) and [A] after the flush of this item overlapped with the
 // velocity-tile load of the CTA's next item (disjoint shared-memory regions).
-__global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, const float4* __restrict__ bounds_in,
+__global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,
                                                                  float4* __restrict__ bounds_out,
                                                                  int* __restrict__ item_box) {
   extern __shared__ float smem[];
@@ -903,9 +903,11 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
     __syncthreads();  // [B] scatter complete; velocity tile free
     FPROF_MARK_DEP(tb1, *(volatile int*)&boxes[par][0]);
     const int x0 = box[0], x1 = box[3] + 2, y0 = box[1], y1 = box[4] + 2, z0 = box[2], z1 = box[5] + 2;
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
       item_box[wi] = x1 - 2 < x0 ? 0x00000FFF
                                  : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
+      bounds_in[wi] = make_float4(0.f, 0.f, 0.f, 0.f);  // consumed: zero for its next use as bounds_out
+    }
     // the CTA's next item: velocity-tile copies issued before the flush so
     // their L2 latency hides under it
     const int wnext = nxt_wi;
@@ -1033,7 +1035,7 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
 }
 
 template <bool DENSE>
-__global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params p, Colliders cs, int clear) {
+__global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params p, Colliders cs, int clear, int* done) {
   // one table for the whole grid: the fp32 prefilter boxes are staged in
   // shared memory once per CTA (per-environment tables use collider_near)
   __shared__ ColliderNearF nf_s[MAX_COLLIDERS];
@@ -1048,11 +1050,15 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   const long long stride = (long long)gridDim.x * (blockDim.x >> 5);
   const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
   long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (it >= nitems) return;
   // one brick per warp iteration (lane -> nodes lane, lane + 32); the next
   // brick's momentum is loaded before this one is processed
-  long long b = DENSE ? it : (long long)p.active_list[it];
-  float4 a0 = p.gm[(b << 6) | lane], a1 = p.gm[((b << 6) | lane) + 32];
+  long long b = 0;
+  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+  if (it < nitems) {
+    b = DENSE ? it : (long long)p.active_list[it];
+    a0 = p.gm[(b << 6) | lane];
+    a1 = p.gm[((b << 6) | lane) + 32];
+  }
   for (; it < nitems; it += stride) {
     const long long nit = it + stride;
     long long nb = b;
@@ -1077,6 +1083,20 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
     b = nb;
     a0 = n0;
     a1 = n1;
+  }
+  // clearing launch of the fast path: the last CTA out zeroes the brick-list
+  // and work-item counters for the next substep (no memset nodes per substep)
+  if (done) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+        *p.active_count = 0;
+        *p.work_next = 0;
+        *done = 0;
+        __threadfence();
+      }
+    }
   }
 }
 

@@ -122,10 +122,12 @@ struct mpm_ctx {
   // CUDA graphs of whole fast-path frames, keyed by the host-side start state
   struct GraphEntry {
     int nsub, col, cur, border, dirty, timing;
+    bool cclean, bclean;  // counters / bounds_out known zero at the start
     long long n;
     long long kernels;  // kernel nodes in the graph (evidence counter)
     cudaGraphExec_t exec;
     int end_cur, end_border, end_dirty;
+    bool end_cclean, end_bclean;
     std::vector<Mark> marks;  // event nodes captured inside the graph
   };
   std::vector<GraphEntry> graphs;
@@ -135,6 +137,8 @@ struct mpm_ctx {
   double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
   int items_per_sm = 4;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
+  bool counters_clean = true;     // counters[0] (active bricks) and [3] (work_next) known zero
+  bool bounds_out_clean = false;  // item_bounds2 known zero
 };
 
 namespace {
@@ -470,8 +474,14 @@ int rebin(mpm_ctx* ctx) {
 // g2p=true: the fused steady-state kernel (bounds of the previous substep).
 int launch_fused(mpm_ctx* ctx, bool g2p) {
   Params p = make_params(ctx);
-  CK(cudaMemsetAsync(ctx->counters, 0, sizeof(int), ctx->stream));
+  // brick-list / work counters: zeroed by the last clearing grid op, else here
+  if (!ctx->counters_clean) {
+    CK(cudaMemsetAsync(ctx->counters, 0, sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(ctx->counters + 3, 0, sizeof(int), ctx->stream));
+  }
+  ctx->counters_clean = false;
   if (!g2p || ctx->split_mode) {
+    ctx->bounds_out_clean = false;
     CK(cudaMemsetAsync(ctx->item_bounds, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
     {
       TimedRegion tr(ctx, 0);
@@ -492,8 +502,11 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
     return 0;
   }
   // fused: bounds_in = item_bounds (last substep), bounds_out = item_bounds2, then swap
-  CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
-  CK(cudaMemsetAsync(ctx->counters + 3, 0, sizeof(int), ctx->stream));
+  // (the kernel zeroes each bounds_in entry it consumes, so after one steady
+  // launch both buffers stay clean)
+  if (!ctx->bounds_out_clean)
+    CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
+  ctx->bounds_out_clean = true;
   {
     TimedRegion tr(ctx, 5);
     fused_kernel<<<ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
@@ -508,11 +521,13 @@ int launch_grid_op(mpm_ctx* ctx, bool dense, bool use_col, int row, bool clear) 
   Params p = make_params(ctx);
   Colliders cs = make_colliders(ctx, row, use_col);
   TimedRegion tr(ctx, 1);
+  int* done = clear && !dense ? ctx->counters + 63 : nullptr;  // counters reset by the last CTA
   if (dense)
-    grid_op_kernel<true><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
+    grid_op_kernel<true><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0, done);
   else
-    grid_op_kernel<false><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0);
+    grid_op_kernel<false><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0, done);
   LAUNCHED();
+  if (done) ctx->counters_clean = true;
   return 0;
 }
 
@@ -778,6 +793,7 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
     TRY(dalloc(ctx, &ctx->item_bounds, (size_t)ctx->work_cap));
     TRY(dalloc(ctx, &ctx->item_bounds2, (size_t)ctx->work_cap));
     ctx->bounds_a = ctx->item_bounds;
+    ctx->bounds_out_clean = false;
     TRY(dalloc(ctx, &ctx->pay, (size_t)cap * NPAY));
     TRY(dalloc(ctx, &ctx->item_box, (size_t)ctx->work_cap));
     if (ctx->perm) {
@@ -1061,7 +1077,8 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
     mpm_ctx::GraphEntry* hit = nullptr;
     for (auto& g : ctx->graphs)
       if (g.nsub == nsub && g.col == (int)col && g.cur == ctx->cur && g.border == border &&
-          g.dirty == ctx->grid_dirty && g.timing == timing && g.n == ctx->n)
+          g.dirty == ctx->grid_dirty && g.timing == timing && g.n == ctx->n && g.cclean == ctx->counters_clean &&
+          g.bclean == ctx->bounds_out_clean)
         hit = &g;
     if (!hit) {
       mpm_ctx::GraphEntry e{};
@@ -1072,6 +1089,8 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       e.dirty = ctx->grid_dirty;
       e.timing = timing;
       e.n = ctx->n;
+      e.cclean = ctx->counters_clean;
+      e.bclean = ctx->bounds_out_clean;
       const size_t marks0 = ctx->marks.size();
       const long long launches0 = ctx->launches;
       CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -1100,11 +1119,15 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       e.end_cur = ctx->cur;
       e.end_border = ctx->item_bounds == ctx->bounds_a ? 0 : 1;
       e.end_dirty = ctx->grid_dirty;
+      e.end_cclean = ctx->counters_clean;
+      e.end_bclean = ctx->bounds_out_clean;
       // the capture advanced the host state as a real run would; restore the
       // start state so the replay below applies the same transition
       ctx->cur = e.cur;
       if ((ctx->item_bounds == ctx->bounds_a ? 0 : 1) != e.border) std::swap(ctx->item_bounds, ctx->item_bounds2);
       ctx->grid_dirty = e.dirty;
+      ctx->counters_clean = e.cclean;
+      ctx->bounds_out_clean = e.bclean;
       ctx->graphs.push_back(std::move(e));
       hit = &ctx->graphs.back();
     }
@@ -1113,6 +1136,8 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
     ctx->cur = hit->end_cur;
     if ((ctx->item_bounds == ctx->bounds_a ? 0 : 1) != hit->end_border) std::swap(ctx->item_bounds, ctx->item_bounds2);
     ctx->grid_dirty = hit->end_dirty;
+    ctx->counters_clean = hit->end_cclean;
+    ctx->bounds_out_clean = hit->end_bclean;
     if (timing)
       for (auto& mk : hit->marks) ctx->marks.push_back(mk);
   }
@@ -1444,6 +1469,7 @@ int mpm_reserve(mpm_ctx* ctx, int64_t cap) {
   TRY(dalloc(ctx, &ctx->item_bounds, (size_t)ctx->work_cap));
   TRY(dalloc(ctx, &ctx->item_bounds2, (size_t)ctx->work_cap));
   ctx->bounds_a = ctx->item_bounds;
+  ctx->bounds_out_clean = false;
   TRY(dalloc(ctx, &ctx->pay, (size_t)cap * NPAY));
   TRY(dalloc(ctx, &ctx->item_box, (size_t)ctx->work_cap));
   if (ctx->perm) {
