@@ -60,6 +60,24 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _ncu_traffic(kernel_prefix: str):
+    """DRAM bytes per launch of the dominant kernel from the newest committed
+    `ncu --set full` summary (profiles/rNN_ncu_<kernel>.json, written by
+    tools/ncu_summary.py from a capture of this bench), or None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_*.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except Exception:
+            continue
+        for rec in d if isinstance(d, list) else [d]:
+            if str(rec.get("kernel", "")).startswith(kernel_prefix) and rec.get("dram_bytes"):
+                best = (rec["dram_bytes"], os.path.relpath(path, ROOT))
+    return best
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -392,6 +410,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_src = _peaks()
+    traffic = _ncu_traffic(dom.split(" ")[0])
     avg_fused_s = fused_ms / fused_n / 1000.0
     achieved = BYTES_PER_PARTICLE_SUBSTEP * n / avg_fused_s / 1e9
     substep_s = t_dev / (args.steps * nsub)
@@ -405,7 +424,9 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed between steps (512 MiB memset)",
                    "wall_s_timed": wall},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
+                     "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                        f"{traffic[1]} (cold-cache ncu replay)") if traffic else None,
                      "kernel": dom,
                      "bytes_per_launch": BYTES_PER_PARTICLE_SUBSTEP * n,
                      "mean_launch_ms": 1000.0 * avg_fused_s, "peak_source": peak_src,
