@@ -52,10 +52,31 @@ constexpr int NF = 26;                    // float fields per particle
 
 enum Field : int { FX = 0, FV = 3, FF = 6, FC = 15, FMASS = 24, FVOL = 25 };
 
+// Division of a non-negative 32-bit value by a runtime-constant divisor with
+// one multiply-high (round-up method: q = (umulhi(n, m) + n) >> s, exact for
+// all n < 2^32), precomputed on the host.
+struct FastDiv {
+  unsigned m;
+  int s;
+  __device__ __forceinline__ unsigned div(unsigned n) const {
+    return (unsigned)(((unsigned long long)__umulhi(n, m) + n) >> s);
+  }
+};
+
+inline FastDiv make_fastdiv(int d) {
+  int l = 0;
+  while ((1LL << l) < d) ++l;
+  FastDiv f;
+  f.m = (unsigned)((((1ULL << 32) * ((1ULL << l) - (unsigned long long)d)) / (unsigned long long)d) + 1);
+  f.s = l;
+  return f;
+}
+
 struct Params {
   // grid
   int res[3];      // node resolution
   int nb[3];       // layout bricks per axis
+  FastDiv fd_nb1, fd_nb2;  // / nb[1], / nb[2]
   int nbin[3];     // particle bins per axis
   float dx, inv_dx, dt;
   float gravity[3];

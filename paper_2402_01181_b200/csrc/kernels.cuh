@@ -21,6 +21,7 @@ namespace mpm {
 #ifdef FUSED_PROFILE
 __device__ unsigned long long g_fprof[6];
 __device__ unsigned long long g_fcnt[4];  // particles, G2P off-tile, P2G fallback
+__device__ unsigned long long g_gprof[8];  // grid op: sum / max CTA ns, CTAs, launches, sum of per-launch max, clearing launches, bricks
 #define FPROF_COUNT(k) atomicAdd(&g_fcnt[k], 1ull)
 #else
 #define FPROF_COUNT(k)
@@ -1039,6 +1040,10 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   // one table for the whole grid: the fp32 prefilter boxes are staged in
   // shared memory once per CTA (per-environment tables use collider_near)
   __shared__ ColliderNearF nf_s[MAX_COLLIDERS];
+#ifdef FUSED_PROFILE
+  unsigned long long g_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
+#endif
   const bool staged = !cs.per_env && cs.theta >= 0.0 && cs.count > 0 && cs.count <= MAX_COLLIDERS;
   if (staged && threadIdx.x < cs.count) nf_s[threadIdx.x] = make_near_f(cs, threadIdx.x, cs.theta_f);
   __syncthreads();
@@ -1049,41 +1054,65 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   const double cap = 2.0 * cs.theta;
   const long long stride = (long long)gridDim.x * (blockDim.x >> 5);
   const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
-  long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  // one brick per warp iteration (lane -> nodes lane, lane + 32); the next
-  // brick's momentum is loaded before this one is processed
-  long long b = 0;
-  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-  if (it < nitems) {
-    b = DENSE ? it : (long long)p.active_list[it];
-    a0 = p.gm[(b << 6) | lane];
-    a1 = p.gm[((b << 6) | lane) + 32];
-  }
-  for (; it < nitems; it += stride) {
-    const long long nit = it + stride;
-    long long nb = b;
-    float4 n0 = a0, n1 = a1;
-    if (nit < nitems) {
-      nb = DENSE ? nit : (long long)p.active_list[nit];
-      n0 = p.gm[(nb << 6) | lane];
-      n1 = p.gm[((nb << 6) | lane) + 32];
+  // this warp's bricks: first, first + stride, ... (strided so that the
+  // expensive contact bricks, clustered in the list, spread over warps).
+  // Their list entries are fetched 32 at a time (one per lane) and the
+  // momentum of the brick after next is loaded while one is processed.
+  const long long first = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nmine = nitems > first ? (nitems - first + stride - 1) / stride : 0;
+  for (long long base = 0; base < nmine; base += 32) {
+    const int cnt = (int)min(32LL, nmine - base);
+    const long long my_it = first + (base + lane) * stride;
+    const int myb = lane < cnt ? (DENSE ? (int)my_it : p.active_list[my_it]) : 0;
+    long long b0 = __shfl_sync(0xffffffffu, myb, 0), b1 = __shfl_sync(0xffffffffu, myb, cnt > 1 ? 1 : 0);
+    float4 a00 = p.gm[(b0 << 6) | lane], a01 = p.gm[((b0 << 6) | lane) + 32];
+    float4 a10 = a00, a11 = a01;
+    if (cnt > 1) {
+      a10 = p.gm[(b1 << 6) | lane];
+      a11 = p.gm[((b1 << 6) | lane) + 32];
     }
-    const int b32 = (int)b;
-    const int bk = b32 % p.nb[2], bj = (b32 / p.nb[2]) % p.nb[1], bi = b32 / (p.nb[2] * p.nb[1]);
-    const long long i0 = (b << 6) | lane, i1 = i0 + 32;
-    const float4 o0 = grid_node(p, cs, nf, single_env, cap, a0, bi * 4 + li0, bj * 4 + lj, bk * 4 + lk);
-    const float4 o1 = grid_node(p, cs, nf, single_env, cap, a1, bi * 4 + li0 + 2, bj * 4 + lj, bk * 4 + lk);
-    p.gv[i0] = o0;
-    p.gv[i1] = o1;
-    if (clear) {
-      p.gm[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
-      p.gm[i1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < cnt; ++k) {
+      long long b2 = b1;
+      float4 a20 = a10, a21 = a11;
+      if (k + 2 < cnt) {
+        b2 = __shfl_sync(0xffffffffu, myb, k + 2);
+        a20 = p.gm[(b2 << 6) | lane];
+        a21 = p.gm[((b2 << 6) | lane) + 32];
+      }
+      const unsigned t12 = p.fd_nb2.div((unsigned)b0);
+      const int bk = (int)((unsigned)b0 - t12 * p.nb[2]);
+      const int bi = (int)p.fd_nb1.div(t12), bj = (int)t12 - bi * p.nb[1];
+      const long long i0 = (b0 << 6) | lane, i1 = i0 + 32;
+      const float4 o0 = grid_node(p, cs, nf, single_env, cap, a00, bi * 4 + li0, bj * 4 + lj, bk * 4 + lk);
+      const float4 o1 = grid_node(p, cs, nf, single_env, cap, a01, bi * 4 + li0 + 2, bj * 4 + lj, bk * 4 + lk);
+      p.gv[i0] = o0;
+      p.gv[i1] = o1;
+      if (clear) {
+        p.gm[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        p.gm[i1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (lane == 0) p.brick_flag[b0] = 0;
+      b0 = b1;
+      a00 = a10;
+      a01 = a11;
+      b1 = b2;
+      a10 = a20;
+      a11 = a21;
     }
-    if (lane == 0) p.brick_flag[b] = 0;
-    b = nb;
-    a0 = n0;
-    a1 = n1;
   }
+#ifdef FUSED_PROFILE
+  {
+    __syncthreads();
+    unsigned long long g_t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t1));
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_gprof[0], g_t1 - g_t0);
+      atomicMax(&g_gprof[1], g_t1 - g_t0);
+      atomicAdd(&g_gprof[2], 1ull);
+      if (blockIdx.x == 0) atomicAdd(&g_gprof[3], 1ull);
+    }
+  }
+#endif
   // clearing launch of the fast path: the last CTA out zeroes the brick-list
   // and work-item counters for the next substep (no memset nodes per substep)
   if (done) {
@@ -1091,6 +1120,11 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
     if (threadIdx.x == 0) {
       __threadfence();
       if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+#ifdef FUSED_PROFILE
+        atomicAdd(&g_gprof[4], atomicExch(&g_gprof[1], 0ull));
+        atomicAdd(&g_gprof[5], 1ull);
+        atomicAdd(&g_gprof[6], (unsigned long long)*p.active_count);
+#endif
         *p.active_count = 0;
         *p.work_next = 0;
         *done = 0;

@@ -266,6 +266,8 @@ Params make_params(mpm_ctx* ctx) {
   for (int a = 0; a < 3; ++a) {
     p.res[a] = c.res[a];
     p.nb[a] = (c.res[a] + 3) / 4;
+    if (a == 1) p.fd_nb1 = make_fastdiv(p.nb[1]);
+    if (a == 2) p.fd_nb2 = make_fastdiv(p.nb[2]);
     p.nbin[a] = ctx->nbin[a];
     p.gravity[a] = (float)c.gravity[a];
     const int et = c.env_tiles[a] > 1 ? c.env_tiles[a] : 1;
@@ -701,6 +703,12 @@ int mpm_destroy(mpm_ctx* ctx) {
     const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
     fprintf(stderr, "[fused profile] warp-cycles: particles %.3f  wait[B] %.3f  flush %.3f  next-tile %.3f  wait[A] %.3f  (total %.3e, ctas %llu)\n",
             h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, tot, h[5]);
+    unsigned long long g[8];
+    cudaMemcpyFromSymbol(g, g_gprof, sizeof(g));
+    if (g[3])
+      fprintf(stderr, "[grid profile] launches %llu  mean CTA %.2f us  mean per-launch max CTA %.2f us (clearing launches %llu, bricks/launch %.0f)  CTAs/launch %llu\n",
+              g[3], g[0] / (double)(g[2] ? g[2] : 1) / 1e3, g[4] / (double)(g[5] ? g[5] : 1) / 1e3, g[5],
+              g[6] / (double)(g[5] ? g[5] : 1), g[2] / g[3]);
     unsigned long long c[4];
     cudaMemcpyFromSymbol(c, g_fcnt, sizeof(c));
     fprintf(stderr, "[fused profile] particles %llu  g2p off-tile %llu (%.4f)  p2g fallback %llu (%.4f, bound %llu)\n",
