@@ -168,6 +168,26 @@ int mpm_download_rows(mpm_ctx *ctx, int32_t *ids, double *x, double *v, double *
 int mpm_collision_field(mpm_ctx *ctx, double theta, double *dist, int32_t *obj);
 /* SimState.has_nan (core.py:149-151) on device. */
 int mpm_has_nan(mpm_ctx *ctx, int *flag);
+
+/* compute_metrics (scene.py:204-220) as a device reduction: out[5] =
+ * {lifted_fraction (dy > 2 dx), detached_fraction (dy > dx),
+ *  mean |det F - 1|, max |x - x0|, particle count}.  x0: the caller's
+ * (n, 3) fp64 reference positions in caller order, uploaded into the context;
+ * NULL reuses the last upload (MPM_ESTATE if none for this particle count). */
+int mpm_metrics(mpm_ctx *ctx, const double *x0, double dx, double *out);
+
+/* splat_density (surfacing.py:45-67 -> kernels.splat_mass / splat_reduce,
+ * kernels.py:541-588): quadratic B-spline mass deposit on a dense res[0] x
+ * res[1] x res[2] lattice of spacing field_dx, divided by field_dx^3; out is
+ * the (res0, res1, res2) C-order fp64 density.  positions == NULL: the
+ * context's particles (no download); else caller (n, 3) positions + (n,)
+ * masses.  fp64 weights, fp64 atomic accumulation (node sums in arrival
+ * order, not the reference's chunk order). */
+int mpm_splat_density(mpm_ctx *ctx, const double *positions, const double *masses, int64_t n,
+                      const int32_t *res, double field_dx, double *out);
+/* Same without a simulation context (temporary device buffers on `device`). */
+int mpm_splat_density_host(int device, const double *positions, const double *masses, int64_t n,
+                           const int32_t *res, double field_dx, double *out);
 /* Per-kernel CUDA-event timing on the context stream (bench/roofline).
  * When enabled every fast-path launch is bracketed by events; mpm_get_timing
  * fills out[14] = {g2p_stress_ms, g2p_stress_launches, grid_op_ms,

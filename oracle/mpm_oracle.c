@@ -733,3 +733,62 @@ void orc32_p2g_sorted(long n, const int64_t *order, const float *x, const float 
   }
   if (inverted) *inverted = inv;
 }
+
+/* ------------------------------------------------------------------------- */
+/* density splat (kernels.py:541-588, surfacing.py:45-67)                    */
+/* ------------------------------------------------------------------------- */
+
+/* kernels.splat_mass: chunk c deposits particles [c n / nchunks, (c + 1) n /
+ * nchunks) into its private buffer, same expression order (weights
+ * 0.5 * (t * t), w_ij = w_i * w_j, w = w_ij * w_k, buf += w * m).  The
+ * reference does not bounds-check; nodes outside the lattice are skipped. */
+void orc_splat_mass(long n, const double *x, const double *mass, double dx, int nx, int ny, int nz,
+                    double *buf, int nchunks) {
+  const double inv_dx = 1.0 / dx;
+  const long nn = (long)nx * ny * nz;
+#pragma omp parallel for schedule(static, 1)
+  for (int c = 0; c < nchunks; ++c) {
+    const long lo = (long)c * n / nchunks, hi = (long)(c + 1) * n / nchunks;
+    double *cb = buf + (size_t)c * nn;
+    for (long p = lo; p < hi; ++p) {
+      double g[3], w[3][3];
+      long b[3];
+      for (int a = 0; a < 3; ++a) {
+        g[a] = x[3 * p + a] * inv_dx;
+        b[a] = (long)floor(g[a] - 0.5);
+        const double f = g[a] - (double)b[a];
+        w[a][0] = 0.5 * ((1.5 - f) * (1.5 - f));
+        w[a][1] = 0.75 - (f - 1.0) * (f - 1.0);
+        w[a][2] = 0.5 * ((f - 0.5) * (f - 0.5));
+      }
+      const double m = mass[p];
+      for (int i = 0; i < 3; ++i) {
+        const long xi = b[0] + i;
+        for (int j = 0; j < 3; ++j) {
+          const long yj = b[1] + j;
+          const double wij = w[0][i] * w[1][j];
+          for (int k = 0; k < 3; ++k) {
+            const long zk = b[2] + k;
+            if (xi < 0 || xi >= nx || yj < 0 || yj >= ny || zk < 0 || zk >= nz) continue;
+            const double wt = wij * w[2][k];
+            cb[(xi * ny + yj) * nz + zk] += wt * m;
+          }
+        }
+      }
+    }
+  }
+}
+
+/* kernels.splat_reduce: node sums in chunk order 0..nchunks-1 from 0.0,
+ * times 1/dx^3; buffers re-zeroed. */
+void orc_splat_reduce(double *buf, double *out, long nn, int nchunks, double inv_cell_volume) {
+#pragma omp parallel for schedule(static)
+  for (long node = 0; node < nn; ++node) {
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+      s += buf[(size_t)c * nn + node];
+      buf[(size_t)c * nn + node] = 0.0;
+    }
+    out[node] = s * inv_cell_volume;
+  }
+}

@@ -230,3 +230,32 @@ def sorted_order(x32, dx, res):
     b = np.clip(b, 0, np.asarray(res) - 3)
     key = (b[:, 0] * res[1] + b[:, 1]) * res[2] + b[:, 2]
     return np.lexsort((np.arange(len(x32)), key))
+
+
+def splat_density(positions, masses, res, dx, chunks: int = 8):
+    """surfacing.splat_density (surfacing.py:45-67 -> kernels.py:541-588):
+    dense (res0, res1, res2) fp64 mass density, chunked like the reference."""
+    res = tuple(int(r) for r in res)
+    nn = res[0] * res[1] * res[2]
+    pos = _c64(positions).reshape(-1, 3)
+    m = _c64(masses).reshape(-1)
+    buf = np.zeros((chunks, nn))
+    out = np.zeros(res)
+    L = lib()
+    if len(pos):
+        L.orc_splat_mass(ctypes.c_long(len(pos)), _p(pos), _p(m), ctypes.c_double(dx), res[0], res[1], res[2],
+                         _p(buf), ctypes.c_int(chunks))
+    L.orc_splat_reduce(_p(buf), _p(out), ctypes.c_long(nn), ctypes.c_int(chunks), ctypes.c_double(1.0 / dx ** 3))
+    return out
+
+
+def compute_metrics(x, F, x0, dx):
+    """scene.compute_metrics (scene.py:204-220), the same numpy expressions:
+    (lifted_fraction, detached_fraction, mean |det F - 1|, max displacement)."""
+    x = np.asarray(x, dtype=np.float64)
+    x0 = np.asarray(x0, dtype=np.float64)
+    dy = x[:, 1] - x0[:, 1]
+    j = np.linalg.det(np.asarray(F, dtype=np.float64))
+    disp = np.linalg.norm(x - x0, axis=1)
+    return (float((dy > 2.0 * dx).mean()), float((dy > dx).mean()), float(np.abs(j - 1.0).mean()),
+            float(disp.max() if len(disp) else 0.0))

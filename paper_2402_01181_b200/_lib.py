@@ -38,7 +38,7 @@ EXPORTS = (
     "mpm_stage_begin", "mpm_stage_particles", "mpm_stage_grid", "mpm_stage_end", "mpm_halo_pack",
     "mpm_halo_unpack_add", "mpm_halo_pack_vel", "mpm_halo_unpack_vel", "mpm_extract_migrants",
     "mpm_append_particles", "mpm_reserve", "mpm_download_ids", "mpm_device_copy", "mpm_set_ids",
-    "mpm_download_rows",
+    "mpm_download_rows", "mpm_metrics", "mpm_splat_density", "mpm_splat_density_host",
 )
 
 
@@ -119,6 +119,9 @@ def lib():
     L.mpm_device_copy.argtypes = [_VP, _VP, ctypes.c_int64]
     L.mpm_set_ids.argtypes = [_VP, _I32]
     L.mpm_download_rows.argtypes = [_VP, _I32, _D, _D, _D, _D]
+    L.mpm_metrics.argtypes = [_VP, _D, ctypes.c_double, _D]
+    L.mpm_splat_density.argtypes = [_VP, _D, _D, ctypes.c_int64, _I32, ctypes.c_double, _D]
+    L.mpm_splat_density_host.argtypes = [ctypes.c_int, _D, _D, ctypes.c_int64, _I32, ctypes.c_double, _D]
     _lib = L
     return L
 

@@ -26,7 +26,12 @@ constexpr int BIN_SHIFT = 3;
 #define MPM_MARGIN 2
 #endif
 constexpr int MARGIN = MPM_MARGIN;        // tile margin for particles drifting out of their bin
-constexpr int TILE = BIN + 2 + 2 * MARGIN;  // 14 nodes per tile edge
+#ifndef MPM_TILE
+#define MPM_TILE (BIN + 2 + 2 * MPM_MARGIN)
+#endif
+// nodes per tile edge (14): base cells org + [0, TILE - 3], i.e. drift of
+// MARGIN - 1 cells below the bin and TILE - BIN - 1 - MARGIN above
+constexpr int TILE = MPM_TILE;
 constexpr int TILE_NODES = TILE * TILE * TILE;
 constexpr int FUSED_THREADS = 256;      // stage A (g2p_stress_kernel)
 #ifndef MPM_FUSED_THREADS

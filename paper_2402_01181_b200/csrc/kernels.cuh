@@ -1583,6 +1583,116 @@ __global__ void has_nan_kernel(Params p, int* flag) {
 }
 
 // ---------------------------------------------------------------------------
+// frame-level consumers of the state: metrics and density splat
+// ---------------------------------------------------------------------------
+
+// compute_metrics (scene.py:204-220) without a particle download: per block
+// {lifted count, detached count, sum |det F - 1|, max |x - x0|} in fp64 over
+// a fixed grid-stride partition (block partials are summed on the host in
+// block order).  x0 is in the caller's order, indexed by original id.
+constexpr int METRICS_THREADS = 256;
+
+__global__ void __launch_bounds__(METRICS_THREADS) metrics_kernel(Params p, const double* __restrict__ x0, double dx,
+                                                                  double* __restrict__ part) {
+  double sum = 0.0, mx = 0.0, c_lift = 0.0, c_det = 0.0;
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n;
+       s += (long long)gridDim.x * blockDim.x) {
+    const long long id = p.orig[s];
+    const double d0 = (double)ldf(p, FX, s) - x0[3 * id], d1 = (double)ldf(p, FX + 1, s) - x0[3 * id + 1],
+                 d2 = (double)ldf(p, FX + 2, s) - x0[3 * id + 2];
+    c_lift += d1 > 2.0 * dx ? 1.0 : 0.0;
+    c_det += d1 > dx ? 1.0 : 0.0;
+    double F[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) F[q] = (double)ldf(p, FF + q, s);
+    const double det = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                       F[2] * (F[3] * F[7] - F[4] * F[6]);
+    sum += fabs(det - 1.0);
+    mx = fmax(mx, sqrt(d0 * d0 + d1 * d1 + d2 * d2));
+  }
+  // fixed-order reduction: warp shuffles, then warps in index order
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_down_sync(0xffffffffu, sum, o);
+    c_lift += __shfl_down_sync(0xffffffffu, c_lift, o);
+    c_det += __shfl_down_sync(0xffffffffu, c_det, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double red[METRICS_THREADS / 32][4];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[w][0] = c_lift;
+    red[w][1] = c_det;
+    red[w][2] = sum;
+    red[w][3] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < METRICS_THREADS / 32; ++k) {
+      r[0] += red[k][0];
+      r[1] += red[k][1];
+      r[2] += red[k][2];
+      r[3] = fmax(r[3], red[k][3]);
+    }
+    for (int k = 0; k < 4; ++k) part[4 * blockIdx.x + k] = r[k];
+  }
+}
+
+// splat_mass (kernels.py:541-576): quadratic B-spline mass deposit on a
+// dense (rx, ry, rz) lattice of spacing 1/inv_dx, C order.  fp64 weights and
+// fp64 atomic accumulation (partition of unity to ~1e-16, so the field
+// integrates to the total mass); the caller scales by 1/dx^3
+// (splat_reduce, kernels.py:579-588).  Source: the context's fp32
+// particles (pos == nullptr) or caller fp64 arrays.  Nodes outside the
+// lattice are skipped (the reference does not bounds-check).
+__global__ void splat_kernel(Params p, const double* __restrict__ pos, const double* __restrict__ mass, long long n,
+                             int rx, int ry, int rz, double inv_dx, double* __restrict__ out) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double g[3], m;
+  if (pos) {
+    g[0] = pos[3 * s] * inv_dx;
+    g[1] = pos[3 * s + 1] * inv_dx;
+    g[2] = pos[3 * s + 2] * inv_dx;
+    m = mass[s];
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = (double)ldf(p, FX + a, s) * inv_dx;
+    m = (double)ldf(p, FMASS, s);
+  }
+  int b[3];
+  double w[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b[a] = (int)floor(g[a] - 0.5);
+    const double f = g[a] - b[a];
+    w[a][0] = 0.5 * ((1.5 - f) * (1.5 - f));
+    w[a][1] = 0.75 - (f - 1.0) * (f - 1.0);
+    w[a][2] = 0.5 * ((f - 0.5) * (f - 0.5));
+  }
+  for (int i = 0; i < 3; ++i) {
+    const int xi = b[0] + i;
+    if (xi < 0 || xi >= rx) continue;
+    for (int j = 0; j < 3; ++j) {
+      const int yj = b[1] + j;
+      if (yj < 0 || yj >= ry) continue;
+      const double wij = w[0][i] * w[1][j];
+      const long long row = ((long long)xi * ry + yj) * rz;
+      for (int k = 0; k < 3; ++k) {
+        const int zk = b[2] + k;
+        if (zk < 0 || zk >= rz) continue;
+        atomicAdd(out + row + zk, wij * w[2][k] * m);
+      }
+    }
+  }
+}
+
+__global__ void scale_kernel(double* v, long long n, double s) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] *= s;
+}
+
+// ---------------------------------------------------------------------------
 // slab decomposition (config 5): sparse ghost-brick exchange + migration
 // ---------------------------------------------------------------------------
 

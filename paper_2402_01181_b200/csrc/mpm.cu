@@ -91,6 +91,8 @@ struct mpm_ctx {
   double* stage = nullptr;
   size_t stage_bytes = 0;
   int* flag = nullptr;
+  double* x0 = nullptr;  // compute_metrics reference positions (caller order)
+  long long x0_n = -1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int fused_blocks = 0;
 
@@ -721,7 +723,7 @@ int mpm_destroy(mpm_ctx* ctx) {
                   ctx->h_recv_data[1], ctx->h_local_ids[0], ctx->h_local_ids[1],
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
-                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag};
+                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag, ctx->x0};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int* b : ctx->scan_tmp)
@@ -1204,6 +1206,109 @@ int mpm_has_nan(mpm_ctx* ctx, int* flag) {
   CK(cudaMemcpyAsync(flag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
+}
+
+int mpm_metrics(mpm_ctx* ctx, const double* x0, double dx, double* out) {
+  if (!ctx || !out) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  for (int k = 0; k < 5; ++k) out[k] = 0.0;
+  out[4] = (double)ctx->n;
+  if (ctx->n <= 0) return 0;
+  if (x0) {
+    if (ctx->x0_n != ctx->n) {
+      TRY(dalloc(ctx, &ctx->x0, (size_t)ctx->n * 3));
+      ctx->x0_n = ctx->n;
+    }
+    CK(cudaMemcpyAsync(ctx->x0, x0, sizeof(double) * 3 * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+  } else if (ctx->x0_n != ctx->n) {
+    return fail(ctx, MPM_ESTATE, "metrics: no initial positions uploaded for this particle count");
+  }
+  const int blocks = ctx->sms * 4;
+  std::vector<double> part((size_t)blocks * 4);
+  TRY(ensure_stage(ctx, sizeof(double) * part.size()));
+  Params p = make_params(ctx);
+  metrics_kernel<<<blocks, METRICS_THREADS, 0, ctx->stream>>>(p, ctx->x0, dx, ctx->stage);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(part.data(), ctx->stage, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double r[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b = 0; b < blocks; ++b) {
+    r[0] += part[4 * b];
+    r[1] += part[4 * b + 1];
+    r[2] += part[4 * b + 2];
+    r[3] = std::max(r[3], part[4 * b + 3]);
+  }
+  const double n = (double)ctx->n;
+  out[0] = r[0] / n;
+  out[1] = r[1] / n;
+  out[2] = r[2] / n;
+  out[3] = r[3];
+  return 0;
+}
+
+namespace {
+int splat_run(mpm_ctx* ctx, int dev, cudaStream_t st, const double* positions, const double* masses, long long n,
+              const int32_t* res, double field_dx, double* out) {
+  const long long nn = (long long)res[0] * res[1] * res[2];
+  double* d_out = nullptr;
+  double* d_pos = nullptr;
+  if (cudaMallocAsync((void**)&d_out, sizeof(double) * std::max(nn, 1LL), st) != cudaSuccess) return MPM_ENOMEM;
+  int rc = 0;
+  if (cudaMemsetAsync(d_out, 0, sizeof(double) * nn, st) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc && n > 0) {
+    Params p{};
+    if (ctx) p = make_params(ctx);
+    const double* dp = nullptr;
+    const double* dm = nullptr;
+    if (positions) {
+      if (cudaMallocAsync((void**)&d_pos, sizeof(double) * 4 * n, st) != cudaSuccess) rc = MPM_ENOMEM;
+      if (!rc && (cudaMemcpyAsync(d_pos, positions, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                  cudaMemcpyAsync(d_pos + 3 * n, masses, sizeof(double) * n, cudaMemcpyHostToDevice, st) != cudaSuccess))
+        rc = MPM_ECUDA;
+      dp = d_pos;
+      dm = d_pos + 3 * n;
+    }
+    if (!rc) {
+      splat_kernel<<<blocks_for(n, 256), 256, 0, st>>>(p, dp, dm, n, res[0], res[1], res[2], 1.0 / field_dx, d_out);
+      if (cudaGetLastError() != cudaSuccess) rc = MPM_ECUDA;
+      if (ctx) ctx->launches++;
+    }
+  }
+  if (!rc && nn > 0) {
+    scale_kernel<<<blocks_for(nn, 256), 256, 0, st>>>(d_out, nn, 1.0 / (field_dx * field_dx * field_dx));
+    if (cudaGetLastError() != cudaSuccess) rc = MPM_ECUDA;
+    if (ctx) ctx->launches++;
+  }
+  if (!rc && cudaMemcpyAsync(out, d_out, sizeof(double) * nn, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = MPM_ECUDA;
+  if (d_pos) cudaFreeAsync(d_pos, st);
+  cudaFreeAsync(d_out, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = MPM_ECUDA;
+  (void)dev;
+  return rc;
+}
+}  // namespace
+
+int mpm_splat_density(mpm_ctx* ctx, const double* positions, const double* masses, int64_t n, const int32_t* res,
+                      double field_dx, double* out) {
+  if (!ctx || !res || !out || !(field_dx > 0.0) || res[0] < 1 || res[1] < 1 || res[2] < 1) return MPM_EINVAL;
+  if (positions && (!masses || n < 0)) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const long long cnt = positions ? n : ctx->n;
+  const int rc = splat_run(ctx, ctx->dev, ctx->stream, positions, masses, cnt, res, field_dx, out);
+  if (rc) return fail(ctx, rc, "splat_density failed");
+  return 0;
+}
+
+int mpm_splat_density_host(int device, const double* positions, const double* masses, int64_t n, const int32_t* res,
+                           double field_dx, double* out) {
+  if (!res || !out || !(field_dx > 0.0) || res[0] < 1 || res[1] < 1 || res[2] < 1 || n < 0) return MPM_EINVAL;
+  if (n > 0 && (!positions || !masses)) return MPM_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return MPM_ECUDA;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return MPM_ECUDA;
+  const int rc = splat_run(nullptr, device, st, positions, masses, n, res, field_dx, out);
+  cudaStreamDestroy(st);
+  return rc;
 }
 
 int mpm_set_timing(mpm_ctx* ctx, int enable) {

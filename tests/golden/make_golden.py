@@ -21,6 +21,9 @@ the reference's own hot-path entry points:
     random state (conftest.random_state-like).
   * kinematics.npz -- scene.pose_at on a rotating keyframe trajectory and
     sampling.sample_box positions for a fixed seed.
+  * frame_ops.npz -- surfacing.splat_density on the test_surfacing blob
+    (sim lattice and a 2x finer one) and scene.compute_metrics on a block
+    after 40 substeps (the frame consumers of SURVEY §8f).
 """
 import os
 import sys
@@ -178,7 +181,31 @@ def kinematics():
                         sample_volume=spawn.rest_volume_per_particle)
 
 
+def frame_ops():
+    grid = sm.Grid(resolution=(16, 16, 16), extent=(1.0, 1.0, 1.0))
+    mats = [sm.Material(1.0e4, 0.3, 1000.0)]
+    spawn = sm.sample_box((0.5, 0.5, 0.5), (0.3, 0.3, 0.3), 4000, seed=21, grid=grid)
+    blob = sm.SimState.from_spawns(grid, [spawn], mats)
+    f16 = sm.splat_density(blob.x, blob.mass, grid)
+    f32 = sm.splat_density(blob.x, blob.mass, grid, resolution=(32, 32, 32))
+    g2 = sm.Grid(resolution=(32, 32, 32), extent=(1.0, 1.0, 1.0))
+    st = sm.SimState.from_spawns(g2, [sm.sample_box((0.5, 0.14, 0.5), (0.3, 0.16, 0.3), 3000, seed=4,
+                                                    grid=g2)], mats)
+    x0 = st.x.copy()
+    params = sm.SimParams()
+    for _ in range(40):
+        sm.substep(st, mats, params)
+    st.x[:200, 1] += 3.0 * g2.dx  # some lifted / detached particles
+    m = sm.compute_metrics(st, x0)
+    np.savez_compressed(os.path.join(OUT, "frame_ops.npz"), blob_x=blob.x, blob_mass=blob.mass,
+                        splat16=f16.values, splat16_dx=f16.dx, splat32=f32.values, splat32_dx=f32.dx,
+                        met_x0=x0, met_x=st.x, met_F=st.F, met_dx=g2.dx,
+                        met=np.array([m.lifted_fraction, m.detached_fraction, m.mean_abs_j_minus_1,
+                                      m.max_displacement]))
+
+
 if __name__ == "__main__":
+    frame_ops()
     substep_colliders()
     floor_block()
     spec_reference()

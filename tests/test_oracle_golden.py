@@ -100,3 +100,19 @@ def test_o3_fp32_sorted_close_to_o1_and_conserves_mass():
                                      g["vol0"], np.zeros(len(order), np.int32), m.mu, m.lam,
                                      5e-4, dx, res, order[::-1].copy())
     assert np.abs(gm2 - gm).max() <= 1e-6 * gm.max()
+
+
+def test_oracle_splat_density_bit_exact():
+    """surfacing.splat_density (kernels.py:541-588) on the test_surfacing blob,
+    on the sim lattice and a 2x finer one."""
+    g = load_golden("frame_ops.npz")
+    for key, res in (("splat16", (16, 16, 16)), ("splat32", (32, 32, 32))):
+        out = O.splat_density(g["blob_x"], g["blob_mass"], res, float(g[f"{key}_dx"]))
+        assert np.array_equal(out, g[key]), key
+    assert np.abs(O.splat_density(np.zeros((0, 3)), np.zeros(0), (16, 16, 16), 1 / 16)).max() == 0.0
+
+
+def test_oracle_compute_metrics_exact():
+    g = load_golden("frame_ops.npz")
+    got = O.compute_metrics(g["met_x"], g["met_F"], g["met_x0"], float(g["met_dx"]))
+    assert np.array_equal(np.array(got), g["met"])
