@@ -577,9 +577,9 @@ int det_p2g(mpm_ctx* ctx) {
   return 0;
 }
 
-int need_particles(mpm_ctx* ctx) {
+int need_particles(mpm_ctx* ctx, bool materials = true) {
   if (ctx->n <= 0) return fail(ctx, MPM_ESTATE, "no particles uploaded");
-  if (ctx->nmat <= 0) return fail(ctx, MPM_ESTATE, "no materials set");
+  if (materials && ctx->nmat <= 0) return fail(ctx, MPM_ESTATE, "no materials set");
   return 0;
 }
 
@@ -1058,7 +1058,7 @@ int mpm_grid_update(mpm_ctx* ctx, int use_colliders) {
 
 int mpm_g2p(mpm_ctx* ctx) {
   if (!ctx) return MPM_EINVAL;
-  TRY(need_particles(ctx));
+  TRY(need_particles(ctx, false));  // g2p_advect (core.py:254-258) takes no materials
   CK(cudaSetDevice(ctx->dev));
   TRY(launch_g2p(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
