@@ -154,18 +154,8 @@ def build_scene(config: str, particles: int | None, seed: int):
 
 def pose_rows(st, cols, params, pose_fn, t0):
     """Per-substep pose table exactly as core.step builds it."""
-    R, T, lv, av, md = [], [], [], [], []
-    t = t0
-    for _ in range(params.substeps_per_frame):
-        pose_fn(cols, t)
-        pk = st._packed_colliders(cols, params)
-        R.append(pk.rotation.copy())
-        T.append(pk.translation.copy())
-        lv.append(pk.linear_velocity.copy())
-        av.append(pk.angular_velocity.copy())
-        md.append(pk.mode.copy())
-        t += params.dt
-    return [np.ascontiguousarray(a) for a in (R, T, lv, av)] + [np.ascontiguousarray(md, np.int32)]
+    from paper_2402_01181_b200.core import pose_table
+    return list(pose_table(st, cols, params, pose_fn, t0))
 
 
 def cpu_oracle_rate(config, particles, seed, substeps, threads):

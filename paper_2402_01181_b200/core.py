@@ -520,6 +520,43 @@ def substep(state: SimState, materials: list[Material], params: SimParams,
     return inv
 
 
+def pose_table(state: SimState, colliders: list[RigidCollider], params: SimParams, pose_fn, t0: float):
+    """Per-substep collider pose table of one frame: ``pose_fn(colliders, t)``
+    at t0, t0 + dt, ... (core.py:296-303; times accumulated like the
+    reference's loop), packed as core.step uploads it.  A ``make_pose_fn``
+    feed evaluates the whole frame at once (scene.PoseFn.table); any other
+    callable is called once per substep."""
+    nsub = params.substeps_per_frame
+    times, t = [], t0
+    for _ in range(nsub):
+        times.append(t)
+        t += params.dt
+    table = getattr(pose_fn, "table", None)
+    if table is None:
+        R, T, lv, av, md = [], [], [], [], []
+        for t in times:
+            pose_fn(colliders, t)
+            pk = state._packed_colliders(colliders, params)
+            R.append(pk.rotation.copy())
+            T.append(pk.translation.copy())
+            lv.append(pk.linear_velocity.copy())
+            av.append(pk.angular_velocity.copy())
+            md.append(pk.mode.copy())
+        return (np.ascontiguousarray(R), np.ascontiguousarray(T), np.ascontiguousarray(lv),
+                np.ascontiguousarray(av), np.ascontiguousarray(md, np.int32))
+    if state._packed is None or state._packed_for != tuple(id(c) for c in colliders):
+        pose_fn(colliders, times[0])  # first pack sees the first substep's modes (F7)
+        state._packed_colliders(colliders, params)
+    R, T, lv, av, modes = table(colliders, times)
+    pk = state._packed_colliders(colliders, params)  # colliders now at the last substep's pose
+    if params.collider_mode == "live":
+        md = np.array([[MODE_NAMES[m] for m in row] for row in modes], dtype=np.int32)
+    else:
+        md = np.repeat(pk.mode[None].astype(np.int32), nsub, axis=0)
+    return (np.ascontiguousarray(R), np.ascontiguousarray(T), np.ascontiguousarray(lv),
+            np.ascontiguousarray(av), np.ascontiguousarray(md, np.int32))
+
+
 def step(state: SimState, materials: list[Material], params: SimParams,
          colliders: list[RigidCollider] | None = None, pose_fn=None) -> StepReport:
     """One frame of ``substeps_per_frame`` substeps (core.py:280-320)."""
@@ -530,19 +567,7 @@ def step(state: SimState, materials: list[Material], params: SimParams,
     if colliders:
         t0 = _time.perf_counter()
         if pose_fn is not None:
-            R, T, lv, av, md = [], [], [], [], []
-            t = state.time
-            for _ in range(nsub):
-                pose_fn(colliders, t)
-                pk = state._packed_colliders(colliders, params)
-                R.append(pk.rotation.copy())
-                T.append(pk.translation.copy())
-                lv.append(pk.linear_velocity.copy())
-                av.append(pk.angular_velocity.copy())
-                md.append(pk.mode.copy())
-                t += params.dt
-            rows = (np.ascontiguousarray(R), np.ascontiguousarray(T), np.ascontiguousarray(lv),
-                    np.ascontiguousarray(av), np.ascontiguousarray(md, np.int32))
+            rows = pose_table(state, colliders, params, pose_fn, state.time)
         else:
             rows = _pose_arrays(state._packed_colliders(colliders, params))
         t_collision += _time.perf_counter() - t0

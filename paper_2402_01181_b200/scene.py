@@ -86,14 +86,108 @@ def apply_poses(colliders, poses, jaw: str, groups: list[GripperGroup] | None = 
             col.mode = "sticky" if jaw == "closed" else (base_mode or {}).get(col.id, "coulomb")
 
 
+def _rotvec_matrix(rv: np.ndarray) -> np.ndarray:
+    """Rotation matrices of rotation vectors (..., 3) (Rodrigues)."""
+    rv = np.asarray(rv, dtype=np.float64)
+    th = np.linalg.norm(rv, axis=-1)
+    safe = np.where(th > 0.0, th, 1.0)
+    k = rv / safe[..., None]
+    K = np.zeros(rv.shape[:-1] + (3, 3))
+    K[..., 0, 1], K[..., 0, 2] = -k[..., 2], k[..., 1]
+    K[..., 1, 0], K[..., 1, 2] = k[..., 2], -k[..., 0]
+    K[..., 2, 0], K[..., 2, 1] = -k[..., 1], k[..., 0]
+    s, c = np.sin(th)[..., None, None], (1.0 - np.cos(th))[..., None, None]
+    R = np.eye(3) + s * K + c * (K @ K)
+    return np.where((th > 0.0)[..., None, None], R, np.eye(3))
+
+
+class _CompiledTrajectory:
+    """pose_at with the per-keyframe / per-segment scipy work done once: a
+    substep pose is a lerp plus R_a exp(s rel) (Rodrigues; equal to scipy's
+    quaternion slerp to ~1e-16).  ``table(times)`` evaluates many substeps in
+    one vectorised pass -- the per-frame pose table core.step uploads."""
+
+    def __init__(self, trajectory: list[Keyframe]):
+        self.times = np.array([k.time for k in trajectory], dtype=np.float64)
+        self.jaw = [k.jaw_state for k in trajectory]
+        self.T = np.array([[np.asarray(T, dtype=np.float64) for T, _ in k.poses] for k in trajectory])
+        rots = [[Rotation.from_quat(_normalized(q)) for _, q in k.poses] for k in trajectory]
+        self.R = np.array([[r.as_matrix() for r in row] for row in rots])
+        nk = len(trajectory)
+        ncol = self.T.shape[1]
+        self.rel = np.zeros((max(nk - 1, 0), ncol, 3))
+        self.av = np.zeros((max(nk - 1, 0), ncol, 3))
+        for i in range(nk - 1):
+            seg = self.times[i + 1] - self.times[i]
+            for c in range(ncol):
+                ra, rb = rots[i][c], rots[i + 1][c]
+                rel = (ra.inv() * rb).as_rotvec()
+                self.rel[i, c] = rel
+                self.av[i, c] = ra.apply(rel) / seg
+
+    def table(self, times):
+        """(R (n, k, 3, 3), T (n, k, 3), lv, av, jaw states) at `times`."""
+        t = np.asarray(times, dtype=np.float64)
+        nk = len(self.times)
+        clamp_lo, clamp_hi = t <= self.times[0], t >= self.times[-1]
+        if nk < 2:
+            n = len(t)
+            return (np.broadcast_to(self.R[0], (n,) + self.R[0].shape).copy(),
+                    np.broadcast_to(self.T[0], (n,) + self.T[0].shape).copy(),
+                    np.zeros((n,) + self.T[0].shape), np.zeros((n,) + self.T[0].shape), [self.jaw[0]] * n)
+        a = np.clip(np.searchsorted(self.times, t, side="right") - 1, 0, nk - 2)
+        seg = self.times[a + 1] - self.times[a]
+        s = ((t - self.times[a]) / seg)[:, None, None]
+        T = (1.0 - s) * self.T[a] + s * self.T[a + 1]
+        R = self.R[a] @ _rotvec_matrix(self.rel[a] * s)
+        lv = (self.T[a + 1] - self.T[a]) / seg[:, None, None]
+        av = self.av[a].copy()
+        for mask, k in ((clamp_lo, 0), (clamp_hi, nk - 1)):
+            if mask.any():
+                R[mask], T[mask], lv[mask], av[mask] = self.R[k], self.T[k], 0.0, 0.0
+        jaw = [self.jaw[0] if clamp_lo[j] else self.jaw[-1] if clamp_hi[j] else self.jaw[a[j]] for j in range(len(t))]
+        return R, T, lv, av, jaw
+
+
+class PoseFn:
+    """``make_pose_fn``'s kinematics feed: ``pose_fn(colliders, t)`` sets the
+    collider poses at time t (scene.py:286-305); ``core.step`` asks it for a
+    whole frame's pose table at once (``table``)."""
+
+    def __init__(self, trajectory, groups=None, base_mode=None):
+        self.trajectory = trajectory
+        self.groups = groups
+        self.base_mode = base_mode
+        self._compiled = _CompiledTrajectory(trajectory)
+
+    def __call__(self, colliders, t):
+        R, T, lv, av, jaw = self._compiled.table([t])
+        poses = [(T[0, c], R[0, c], lv[0, c], av[0, c]) for c in range(T.shape[1])]
+        apply_poses(colliders, poses, jaw[0], self.groups, self.base_mode)
+
+    def table(self, colliders, times):
+        """Per-substep (R, T, lv, av) arrays and the colliders' modes after
+        each pose update (jaw-driven for gripper groups); leaves the colliders
+        at the last time, as the per-substep calls would."""
+        R, T, lv, av, jaw = self._compiled.table(times)
+        grouped = {cid for g in (self.groups or []) for cid in g.colliders}
+        modes = []
+        for j in range(len(times)):
+            row = []
+            for c in colliders:
+                if c.id in grouped:
+                    row.append("sticky" if jaw[j] == "closed" else (self.base_mode or {}).get(c.id, "coulomb"))
+                else:
+                    row.append(c.mode)
+            modes.append(row)
+        last = len(times) - 1
+        self.__call__(colliders, times[last]) if last >= 0 else None
+        return R, T, lv, av, modes
+
+
 def make_pose_fn(trajectory: list[Keyframe], groups: list[GripperGroup] | None = None,
                  base_mode: dict | None = None):
     """Kinematics feed for ``step``: sets collider poses at substep times."""
     if not trajectory:
         return None
-
-    def pose_fn(colliders, t):
-        poses, jaw = pose_at(trajectory, t)
-        apply_poses(colliders, poses, jaw, groups, base_mode)
-
-    return pose_fn
+    return PoseFn(trajectory, groups, base_mode)
