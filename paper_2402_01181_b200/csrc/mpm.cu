@@ -25,6 +25,8 @@ struct mpm_ctx {
   int dev = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t xstream = nullptr;  // host<->device field copies, pipelined with the conversions
+  cudaEvent_t field_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::string err;
   long long launches = 0;
 
@@ -645,6 +647,9 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->dev);
   int rc = 0;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc && cudaStreamCreateWithFlags(&ctx->xstream, cudaStreamNonBlocking) != cudaSuccess) rc = MPM_ECUDA;
+  for (int k = 0; k < 4 && !rc; ++k)
+    if (cudaEventCreateWithFlags(&ctx->field_ev[k], cudaEventDisableTiming) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc) rc = alloc_grid(ctx);
   if (!rc) rc = dalloc(ctx, &ctx->counters, 64);
   if (!rc) rc = dalloc(ctx, &ctx->inverted, 1);
@@ -736,6 +741,9 @@ int mpm_destroy(mpm_ctx* ctx) {
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
+  for (cudaEvent_t e : ctx->field_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return 0;
 }
@@ -834,18 +842,21 @@ int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double
   CK(cudaSetDevice(ctx->dev));
   long long n = ctx->n;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
-  double* sx = ctx->stage;
-  double* sv = sx + 3 * n;
-  double* sF = sx + 6 * n;
-  double* sC = sx + 15 * n;
-  if ((mask & MPM_FIELD_X) && x) CK(cudaMemcpyAsync(sx, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
-  if ((mask & MPM_FIELD_V) && v) CK(cudaMemcpyAsync(sv, v, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
-  if ((mask & MPM_FIELD_F) && F) CK(cudaMemcpyAsync(sF, F, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, ctx->stream));
-  if ((mask & MPM_FIELD_C) && C) CK(cudaMemcpyAsync(sC, C, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, ctx->stream));
-  unsigned m = (x ? mask & 1u : 0u) | (v ? mask & 2u : 0u) | (F ? mask & 4u : 0u) | (C ? mask & 8u : 0u);
+  double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
+  const double* src[4] = {x, v, F, C};
+  const int width[4] = {3, 3, 9, 9};
   Params p = make_params(ctx);
-  upload_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, sx, sv, sF, sC, m);
-  LAUNCHED();
+  // field k's H2D copy (copy stream) overlaps field k-1's conversion
+  CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->xstream, ctx->field_ev[0], 0));  // stage buffer free
+  for (int k = 0; k < 4; ++k) {
+    if (!((mask >> k) & 1u) || !src[k]) continue;
+    CK(cudaMemcpyAsync(st[k], src[k], sizeof(double) * width[k] * n, cudaMemcpyHostToDevice, ctx->xstream));
+    CK(cudaEventRecord(ctx->field_ev[k], ctx->xstream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->field_ev[k], 0));
+    upload_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, st[0], st[1], st[2], st[3], 1u << k);
+    LAUNCHED();
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
@@ -855,18 +866,20 @@ int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, do
   CK(cudaSetDevice(ctx->dev));
   long long n = ctx->n;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
-  double* sx = ctx->stage;
-  double* sv = sx + 3 * n;
-  double* sF = sx + 6 * n;
-  double* sC = sx + 15 * n;
-  unsigned m = (x ? mask & 1u : 0u) | (v ? mask & 2u : 0u) | (F ? mask & 4u : 0u) | (C ? mask & 8u : 0u);
+  double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
+  double* dst[4] = {x, v, F, C};
+  const int width[4] = {3, 3, 9, 9};
   Params p = make_params(ctx);
-  download_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, sx, sv, sF, sC, m);
-  LAUNCHED();
-  if (m & 1u) CK(cudaMemcpyAsync(x, sx, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (m & 2u) CK(cudaMemcpyAsync(v, sv, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (m & 4u) CK(cudaMemcpyAsync(F, sF, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (m & 8u) CK(cudaMemcpyAsync(C, sC, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  // field k's D2H copy (copy stream) overlaps field k+1's conversion
+  for (int k = 0; k < 4; ++k) {
+    if (!((mask >> k) & 1u) || !dst[k]) continue;
+    download_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, st[0], st[1], st[2], st[3], 1u << k);
+    LAUNCHED();
+    CK(cudaEventRecord(ctx->field_ev[k], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->xstream, ctx->field_ev[k], 0));
+    CK(cudaMemcpyAsync(dst[k], st[k], sizeof(double) * width[k] * n, cudaMemcpyDeviceToHost, ctx->xstream));
+  }
+  CK(cudaStreamSynchronize(ctx->xstream));
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
