@@ -1058,7 +1058,10 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   // expensive contact bricks, clustered in the list, spread over warps).
   // Their list entries are fetched 32 at a time (one per lane) and the
   // momentum of the brick after next is loaded while one is processed.
-  const long long first = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // warp-major numbering (warp w of CTA c is w * gridDim + c): consecutive
+  // list entries -- one item's bricks, e.g. a tool's contact band -- land in
+  // different CTAs / SMs instead of the 8 warps of one CTA
+  const long long first = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const long long nmine = nitems > first ? (nitems - first + stride - 1) / stride : 0;
   for (long long base = 0; base < nmine; base += 32) {
     const int cnt = (int)min(32LL, nmine - base);
