@@ -182,6 +182,11 @@ def cpu_oracle_rate(config, particles, seed, substeps, threads):
     return n / dt_med, times[1:], n
 
 
+def scene_workload(config, n, res, ncols):
+    return (f"{config}: {n} particles/GPU, {res}^3 grid, {ncols} tool(s)"
+            + (" pressing 3 cm at 0.5 m/s then holding" if config == "c3" else "") + ", 25 substeps per step")
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -213,8 +218,10 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / len(per),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {n} particles, {g.resolution[0]}^3 grid, "
-                   f"{len(cols)} tool(s)", "particles": n, "grid": list(g.resolution)},
+        "config": {"workload": scene_workload(args.config, n, g.resolution[0], len(cols)),
+                   "particles_per_gpu": n, "grid": list(g.resolution),
+                   "substeps_per_step": params.substeps_per_frame,
+                   "parallelism": f"CPU, {threads} threads (each timed step is one substep of the frame)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"each step = 1 substep of the full {args.config} scene "
                                    f"(O1 fp64 C restatement of kernels.py, 8 chunks, OpenMP)"},
@@ -277,9 +284,7 @@ def run_ours(args, rank, world, local_rank):
         def warm():
             sm.step(st, mats, params, cols, pose_fn)
 
-        workload = (f"{args.config}: {st.particle_count} particles/GPU, {st.grid.resolution[0]}^3 grid, "
-                    f"{len(cols)} tool(s)" + (" pressing 3 cm at 0.5 m/s then holding" if args.config == "c3" else "")
-                    + ", 25 substeps per step")
+        workload = scene_workload(args.config, st.particle_count, st.grid.resolution[0], len(cols))
     if args.rebin:
         params.rebin_interval = args.rebin
     n = st.particle_count
