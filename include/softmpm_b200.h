@@ -185,9 +185,21 @@ int mpm_metrics(mpm_ctx *ctx, const double *x0, double dx, double *out);
  * order, not the reference's chunk order). */
 int mpm_splat_density(mpm_ctx *ctx, const double *positions, const double *masses, int64_t n,
                       const int32_t *res, double field_dx, double *out);
+/* The density field also stays on the device (out may be NULL) as the input
+ * of mpm_marching_cubes(values = NULL). */
 /* Same without a simulation context (temporary device buffers on `device`). */
 int mpm_splat_density_host(int device, const double *positions, const double *masses, int64_t n,
                            const int32_t *res, double field_dx, double *out);
+
+/* marching_cubes (surfacing.py:70-95; scikit-image's Lorensen tables in the
+ * reference) on the device: isosurface at `iso` of the dense fp64 field
+ * (values: host (res0, res1, res2) C-order array, or NULL for the context's
+ * last splatted field).  Indexed mesh, one vertex per crossed lattice edge,
+ * counter-clockwise triangles seen from the outside (value < iso) and unit
+ * outward normals; the counts come back here, the arrays via mpm_mesh_fetch. */
+int mpm_marching_cubes(mpm_ctx *ctx, const double *values, const int32_t *res, double dx, double iso,
+                       int64_t *nverts, int64_t *ntris);
+int mpm_mesh_fetch(mpm_ctx *ctx, double *verts, int32_t *tris, double *normals);
 /* Per-kernel CUDA-event timing on the context stream (bench/roofline).
  * When enabled every fast-path launch is bracketed by events; mpm_get_timing
  * fills out[14] = {g2p_stress_ms, g2p_stress_launches, grid_op_ms,

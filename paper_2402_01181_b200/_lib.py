@@ -39,6 +39,7 @@ EXPORTS = (
     "mpm_halo_unpack_add", "mpm_halo_pack_vel", "mpm_halo_unpack_vel", "mpm_extract_migrants",
     "mpm_append_particles", "mpm_reserve", "mpm_download_ids", "mpm_device_copy", "mpm_set_ids",
     "mpm_download_rows", "mpm_metrics", "mpm_splat_density", "mpm_splat_density_host",
+    "mpm_marching_cubes", "mpm_mesh_fetch",
 )
 
 
@@ -122,6 +123,8 @@ def lib():
     L.mpm_metrics.argtypes = [_VP, _D, ctypes.c_double, _D]
     L.mpm_splat_density.argtypes = [_VP, _D, _D, ctypes.c_int64, _I32, ctypes.c_double, _D]
     L.mpm_splat_density_host.argtypes = [ctypes.c_int, _D, _D, ctypes.c_int64, _I32, ctypes.c_double, _D]
+    L.mpm_marching_cubes.argtypes = [_VP, _D, _I32, ctypes.c_double, ctypes.c_double, _I64, _I64]
+    L.mpm_mesh_fetch.argtypes = [_VP, _D, _I32, _D]
     _lib = L
     return L
 

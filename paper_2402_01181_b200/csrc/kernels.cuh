@@ -15,6 +15,7 @@
 #pragma once
 #include "collide.cuh"
 #include "common.cuh"
+#include "mc_table.h"
 
 namespace mpm {
 
@@ -1693,6 +1694,116 @@ __global__ void splat_kernel(Params p, const double* __restrict__ pos, const dou
 __global__ void scale_kernel(double* v, long long n, double s) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) v[i] *= s;
+}
+
+// Isosurface of a dense (nx, ny, nz) C-order fp64 field (marching cubes,
+// the surfacing step after the splat; surfacing.py:70-95).  Case table:
+// mc_table.h (tools/gen_mc_table.py).  One vertex per crossed lattice edge
+// (edge id = node * 3 + axis, numbered by a scan over the crossing flags), so
+// the mesh is indexed and welded like the reference's; normals are the
+// normalised negative field gradient (central differences, one-sided at the
+// border) interpolated along the edge, i.e. outward from the dense side.
+__device__ __forceinline__ long long mc_node(int i, int j, int k, int ny, int nz) {
+  return ((long long)i * ny + j) * nz + k;
+}
+
+__global__ void mc_edge_flag_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso,
+                                    int* __restrict__ flag) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nn = (long long)nx * ny * nz;
+  if (e >= 3 * nn) return;
+  const long long node = e / 3;
+  const int axis = (int)(e - node * 3);
+  const int k = (int)(node % nz), j = (int)((node / nz) % ny), i = (int)(node / ((long long)ny * nz));
+  const int i2 = i + (axis == 0), j2 = j + (axis == 1), k2 = k + (axis == 2);
+  int c = 0;
+  if (i2 < nx && j2 < ny && k2 < nz) c = (f[node] >= iso) != (f[mc_node(i2, j2, k2, ny, nz)] >= iso);
+  flag[e] = c;
+}
+
+__device__ __forceinline__ void mc_grad(const double* f, int nx, int ny, int nz, int i, int j, int k, double g[3]) {
+  const int ii[3] = {i, j, k}, nn[3] = {nx, ny, nz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    int lo[3] = {i, j, k}, hi[3] = {i, j, k};
+    lo[a] = max(ii[a] - 1, 0);
+    hi[a] = min(ii[a] + 1, nn[a] - 1);
+    const double span = (double)(hi[a] - lo[a]);
+    g[a] = span > 0.0 ? (f[mc_node(hi[0], hi[1], hi[2], ny, nz)] - f[mc_node(lo[0], lo[1], lo[2], ny, nz)]) / span
+                      : 0.0;
+  }
+}
+
+__global__ void mc_edge_vertex_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso, double dx,
+                                      const int* __restrict__ flag, const int* __restrict__ vid,
+                                      double* __restrict__ verts, double* __restrict__ normals) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nn = (long long)nx * ny * nz;
+  if (e >= 3 * nn || !flag[e]) return;
+  const long long node = e / 3;
+  const int axis = (int)(e - node * 3);
+  const int k = (int)(node % nz), j = (int)((node / nz) % ny), i = (int)(node / ((long long)ny * nz));
+  const int i2 = i + (axis == 0), j2 = j + (axis == 1), k2 = k + (axis == 2);
+  const double f0 = f[node], f1 = f[mc_node(i2, j2, k2, ny, nz)];
+  const double t = (iso - f0) / (f1 - f0);
+  const long long v = vid[e];
+  const double p0[3] = {(double)i, (double)j, (double)k}, p1[3] = {(double)i2, (double)j2, (double)k2};
+  double g0[3], g1[3];
+  mc_grad(f, nx, ny, nz, i, j, k, g0);
+  mc_grad(f, nx, ny, nz, i2, j2, k2, g1);
+  double n[3], nrm = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    verts[3 * v + a] = (p0[a] + t * (p1[a] - p0[a])) * dx;
+    n[a] = -(g0[a] + t * (g1[a] - g0[a]));
+    nrm += n[a] * n[a];
+  }
+  nrm = nrm > 1e-60 ? 1.0 / sqrt(nrm) : 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) normals[3 * v + a] = n[a] * nrm;
+}
+
+__device__ __forceinline__ int mc_case(const double* f, int ny, int nz, int i, int j, int k, double iso) {
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int di = (q == 1 || q == 2 || q == 5 || q == 6), dj = (q == 2 || q == 3 || q == 6 || q == 7), dk = q >= 4;
+    c |= (f[mc_node(i + di, j + dj, k + dk, ny, nz)] >= iso) << q;
+  }
+  return c;
+}
+
+__global__ void mc_cell_count_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso,
+                                     int* __restrict__ cnt) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nc = (long long)(nx - 1) * (ny - 1) * (nz - 1);
+  if (c >= nc) return;
+  const int k = (int)(c % (nz - 1)), j = (int)((c / (nz - 1)) % (ny - 1)), i = (int)(c / ((long long)(ny - 1) * (nz - 1)));
+  cnt[c] = MC_NTRI[mc_case(f, ny, nz, i, j, k, iso)];
+}
+
+__global__ void mc_cell_emit_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso,
+                                    const int* __restrict__ cnt, const int* __restrict__ off,
+                                    const int* __restrict__ vid, int* __restrict__ tris) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nc = (long long)(nx - 1) * (ny - 1) * (nz - 1);
+  if (c >= nc || !cnt[c]) return;
+  const int k = (int)(c % (nz - 1)), j = (int)((c / (nz - 1)) % (ny - 1)), i = (int)(c / ((long long)(ny - 1) * (nz - 1)));
+  const int cs = mc_case(f, ny, nz, i, j, k, iso);
+  const int nt = MC_NTRI[cs];
+  const long long o = off[c];
+  for (int q = 0; q < 3 * nt; ++q) {
+    const int e = MC_TRI[cs][q];
+    const int a = MC_EDGE[e][0], b = MC_EDGE[e][1];
+    // lower corner of the edge and its axis
+    const int ca = min(a, b) == a ? a : b;
+    const int ai = (a == 1 || a == 2 || a == 5 || a == 6), aj = (a == 2 || a == 3 || a == 6 || a == 7), ak = a >= 4;
+    const int bi = (b == 1 || b == 2 || b == 5 || b == 6), bj = (b == 2 || b == 3 || b == 6 || b == 7), bk = b >= 4;
+    (void)ca;
+    const int li = min(ai, bi), lj = min(aj, bj), lk = min(ak, bk);
+    const int axis = ai != bi ? 0 : (aj != bj ? 1 : 2);
+    tris[3 * o + q] = vid[mc_node(i + li, j + lj, k + lk, ny, nz) * 3 + axis];
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -94,6 +94,19 @@ struct mpm_ctx {
   size_t stage_bytes = 0;
   int* flag = nullptr;
   double* x0 = nullptr;  // compute_metrics reference positions (caller order)
+  // isosurface: the last device density field and the last extracted mesh
+  double* field = nullptr;
+  long long field_n = 0;
+  int field_res[3] = {0, 0, 0};
+  double field_dx = 0.0;
+  int* mc_flag = nullptr;  // 3 nn crossing flags, then vertex ids
+  int* mc_vid = nullptr;
+  int* mc_cnt = nullptr;  // cells: triangle counts, then offsets
+  int* mc_off = nullptr;
+  long long mc_cap = 0;
+  double* mesh_v = nullptr;  // vertices, then normals
+  int* mesh_t = nullptr;
+  long long mesh_nv = 0, mesh_nt = 0, mesh_vcap = 0, mesh_tcap = 0;
   long long x0_n = -1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int fused_blocks = 0;
@@ -728,7 +741,7 @@ int mpm_destroy(mpm_ctx* ctx) {
                   ctx->h_recv_data[1], ctx->h_local_ids[0], ctx->h_local_ids[1],
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
-                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag, ctx->x0};
+                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag, ctx->x0, ctx->field, ctx->mc_flag, ctx->mc_vid, ctx->mc_cnt, ctx->mc_off, ctx->mesh_v, ctx->mesh_t};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int* b : ctx->scan_tmp)
@@ -1261,11 +1274,11 @@ int mpm_metrics(mpm_ctx* ctx, const double* x0, double dx, double* out) {
 
 namespace {
 int splat_run(mpm_ctx* ctx, int dev, cudaStream_t st, const double* positions, const double* masses, long long n,
-              const int32_t* res, double field_dx, double* out) {
+              const int32_t* res, double field_dx, double* out, double* keep = nullptr) {
   const long long nn = (long long)res[0] * res[1] * res[2];
-  double* d_out = nullptr;
+  double* d_out = keep;
   double* d_pos = nullptr;
-  if (cudaMallocAsync((void**)&d_out, sizeof(double) * std::max(nn, 1LL), st) != cudaSuccess) return MPM_ENOMEM;
+  if (!d_out && cudaMallocAsync((void**)&d_out, sizeof(double) * std::max(nn, 1LL), st) != cudaSuccess) return MPM_ENOMEM;
   int rc = 0;
   if (cudaMemsetAsync(d_out, 0, sizeof(double) * nn, st) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc && n > 0) {
@@ -1292,9 +1305,10 @@ int splat_run(mpm_ctx* ctx, int dev, cudaStream_t st, const double* positions, c
     if (cudaGetLastError() != cudaSuccess) rc = MPM_ECUDA;
     if (ctx) ctx->launches++;
   }
-  if (!rc && cudaMemcpyAsync(out, d_out, sizeof(double) * nn, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = MPM_ECUDA;
+  if (!rc && out && cudaMemcpyAsync(out, d_out, sizeof(double) * nn, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = MPM_ECUDA;
   if (d_pos) cudaFreeAsync(d_pos, st);
-  cudaFreeAsync(d_out, st);
+  if (!keep) cudaFreeAsync(d_out, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) rc = MPM_ECUDA;
   (void)dev;
   return rc;
@@ -1303,12 +1317,105 @@ int splat_run(mpm_ctx* ctx, int dev, cudaStream_t st, const double* positions, c
 
 int mpm_splat_density(mpm_ctx* ctx, const double* positions, const double* masses, int64_t n, const int32_t* res,
                       double field_dx, double* out) {
-  if (!ctx || !res || !out || !(field_dx > 0.0) || res[0] < 1 || res[1] < 1 || res[2] < 1) return MPM_EINVAL;
+  if (!ctx || !res || !(field_dx > 0.0) || res[0] < 1 || res[1] < 1 || res[2] < 1) return MPM_EINVAL;
   if (positions && (!masses || n < 0)) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
   const long long cnt = positions ? n : ctx->n;
-  const int rc = splat_run(ctx, ctx->dev, ctx->stream, positions, masses, cnt, res, field_dx, out);
+  const long long nn = (long long)res[0] * res[1] * res[2];
+  if (ctx->field_n < nn) {
+    TRY(dalloc(ctx, &ctx->field, (size_t)nn));
+    ctx->field_n = nn;
+  }
+  const int rc = splat_run(ctx, ctx->dev, ctx->stream, positions, masses, cnt, res, field_dx, out, ctx->field);
   if (rc) return fail(ctx, rc, "splat_density failed");
+  for (int a = 0; a < 3; ++a) ctx->field_res[a] = res[a];
+  ctx->field_dx = field_dx;
+  return 0;
+}
+
+int mpm_marching_cubes(mpm_ctx* ctx, const double* values, const int32_t* res, double dx, double iso, int64_t* nverts,
+                       int64_t* ntris) {
+  if (!ctx || !nverts || !ntris) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  int r[3];
+  double h = dx;
+  if (values) {
+    if (!res || res[0] < 1 || res[1] < 1 || res[2] < 1 || !(dx > 0.0)) return fail(ctx, MPM_EINVAL, "marching_cubes: bad field");
+    const long long nn = (long long)res[0] * res[1] * res[2];
+    if (ctx->field_n < nn) {
+      TRY(dalloc(ctx, &ctx->field, (size_t)nn));
+      ctx->field_n = nn;
+    }
+    CK(cudaMemcpyAsync(ctx->field, values, sizeof(double) * nn, cudaMemcpyHostToDevice, ctx->stream));
+    for (int a = 0; a < 3; ++a) r[a] = res[a];
+  } else {
+    if (ctx->field_res[0] < 1) return fail(ctx, MPM_ESTATE, "marching_cubes: no device field (splat first)");
+    for (int a = 0; a < 3; ++a) r[a] = ctx->field_res[a];
+    h = ctx->field_dx;
+  }
+  *nverts = 0;
+  *ntris = 0;
+  ctx->mesh_nv = ctx->mesh_nt = 0;
+  if (r[0] < 2 || r[1] < 2 || r[2] < 2) return 0;
+  const long long nn = (long long)r[0] * r[1] * r[2];
+  const long long ne = 3 * nn, nc = (long long)(r[0] - 1) * (r[1] - 1) * (r[2] - 1);
+  if (ne + 1 > INT32_MAX) return fail(ctx, MPM_EINVAL, "marching_cubes: field too large");
+  if (ctx->mc_cap < ne) {
+    TRY(dalloc(ctx, &ctx->mc_flag, (size_t)ne));
+    TRY(dalloc(ctx, &ctx->mc_vid, (size_t)ne));
+    TRY(dalloc(ctx, &ctx->mc_cnt, (size_t)ne));
+    TRY(dalloc(ctx, &ctx->mc_off, (size_t)ne));
+    ctx->mc_cap = ne;
+  }
+  TRY(ensure_scan(ctx, ne));
+  mc_edge_flag_kernel<<<blocks_for(ne, 256), 256, 0, ctx->stream>>>(ctx->field, r[0], r[1], r[2], iso, ctx->mc_flag);
+  LAUNCHED();
+  TRY(scan_exclusive(ctx, ctx->mc_flag, ctx->mc_vid, ne));
+  mc_cell_count_kernel<<<blocks_for(nc, 256), 256, 0, ctx->stream>>>(ctx->field, r[0], r[1], r[2], iso, ctx->mc_cnt);
+  LAUNCHED();
+  TRY(scan_exclusive(ctx, ctx->mc_cnt, ctx->mc_off, nc));
+  int tail[4];
+  CK(cudaMemcpyAsync(tail, ctx->mc_vid + ne - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(tail + 1, ctx->mc_flag + ne - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(tail + 2, ctx->mc_off + nc - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(tail + 3, ctx->mc_cnt + nc - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const long long nv = (long long)tail[0] + tail[1], nt = (long long)tail[2] + tail[3];
+  if (ctx->mesh_vcap < nv) {
+    TRY(dalloc(ctx, &ctx->mesh_v, (size_t)std::max(nv, 1LL) * 6));
+    ctx->mesh_vcap = nv;
+  }
+  if (ctx->mesh_tcap < nt) {
+    TRY(dalloc(ctx, &ctx->mesh_t, (size_t)std::max(nt, 1LL) * 3));
+    ctx->mesh_tcap = nt;
+  }
+  if (nv > 0) {
+    mc_edge_vertex_kernel<<<blocks_for(ne, 256), 256, 0, ctx->stream>>>(ctx->field, r[0], r[1], r[2], iso, h, ctx->mc_flag,
+                                                                       ctx->mc_vid, ctx->mesh_v, ctx->mesh_v + 3 * nv);
+    LAUNCHED();
+  }
+  if (nt > 0) {
+    mc_cell_emit_kernel<<<blocks_for(nc, 256), 256, 0, ctx->stream>>>(ctx->field, r[0], r[1], r[2], iso, ctx->mc_cnt,
+                                                                     ctx->mc_off, ctx->mc_vid, ctx->mesh_t);
+    LAUNCHED();
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->mesh_nv = nv;
+  ctx->mesh_nt = nt;
+  *nverts = nv;
+  *ntris = nt;
+  return 0;
+}
+
+int mpm_mesh_fetch(mpm_ctx* ctx, double* verts, int32_t* tris, double* normals) {
+  if (!ctx) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const long long nv = ctx->mesh_nv, nt = ctx->mesh_nt;
+  if (verts && nv) CK(cudaMemcpyAsync(verts, ctx->mesh_v, sizeof(double) * 3 * nv, cudaMemcpyDeviceToHost, ctx->stream));
+  if (normals && nv)
+    CK(cudaMemcpyAsync(normals, ctx->mesh_v + 3 * nv, sizeof(double) * 3 * nv, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tris && nt) CK(cudaMemcpyAsync(tris, ctx->mesh_t, sizeof(int) * 3 * nt, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 

@@ -8,11 +8,16 @@
   (-> kernels.splat_mass / splat_reduce, kernels.py:541-588): the
   quadratic B-spline mass deposit that feeds marching cubes, on the GPU;
   ``density_field(state, resolution)`` splats a SimState's own particles
-  without downloading them.  Marching cubes itself (scikit-image in the
-  reference, absent from this image) is not provided.
+  without downloading them.
+* ``marching_cubes(field, iso)`` / ``compute_uvs`` / ``extract_surface`` --
+  surfacing.py:70-112: the isosurface on the GPU (case table derived in
+  tools/gen_mc_table.py; the reference calls scikit-image's Lorensen tables,
+  absent here, so triangle-level parity is not pinned -- the tests check the
+  reference's own geometric cases and watertightness); ``extract_surface``
+  splats and triangulates on the device and reads back only the mesh.
 
-Both run through the C ABI (``mpm_metrics``, ``mpm_splat_density[_host]``);
-there is no CPU path.
+All of it runs through the C ABI (``mpm_metrics``, ``mpm_splat_density[_host]``,
+``mpm_marching_cubes``, ``mpm_mesh_fetch``); there is no CPU path.
 """
 
 from __future__ import annotations
@@ -128,3 +133,74 @@ def density_field(state: SimState, resolution: tuple[int, int, int] | None = Non
     ctx.call("mpm_splat_density", _lib.ptr(None), _lib.ptr(None), ctypes.c_int64(0), r, ctypes.c_double(dx),
              _lib.ptr(out))
     return ScalarField(values=out, dx=dx)
+
+
+@dataclass
+class SurfaceMesh:
+    """surfacing.py:29-40."""
+
+    vertices: np.ndarray
+    indices: np.ndarray
+    uvs: np.ndarray | None = None
+    normals: np.ndarray | None = None
+
+    @classmethod
+    def empty(cls) -> "SurfaceMesh":
+        return cls(vertices=np.zeros((0, 3)), indices=np.zeros((0, 3), dtype=np.int32),
+                   uvs=np.zeros((0, 2)), normals=np.zeros((0, 3)))
+
+
+def _fetch_mesh(ctx: _lib.Context, nv: int, nt: int) -> SurfaceMesh:
+    verts = np.zeros((nv, 3))
+    normals = np.zeros((nv, 3))
+    tris = np.zeros((nt, 3), dtype=np.int32)
+    ctx.call("mpm_mesh_fetch", _lib.ptr(verts), _lib.ptr(tris, _lib._I32), _lib.ptr(normals))
+    return SurfaceMesh(vertices=verts, indices=tris, normals=normals)
+
+
+def marching_cubes(fld: ScalarField, iso: float) -> SurfaceMesh:
+    """Isosurface of a density field (surfacing.py:70-95): ParameterError for
+    iso <= 0, an empty mesh when the field never reaches the iso level."""
+    if iso <= 0.0:
+        raise ParameterError("iso level must be positive")
+    values = np.ascontiguousarray(fld.values, dtype=np.float64)
+    vmax = float(values.max()) if values.size else 0.0
+    if vmax < iso or float(values.min()) >= iso:
+        return SurfaceMesh.empty()
+    from .core import _field_ctx
+    ctx = _field_ctx(Grid((8, 8, 8)))
+    r = (ctypes.c_int32 * 3)(*values.shape)
+    nv, nt = ctypes.c_int64(0), ctypes.c_int64(0)
+    ctx.call("mpm_marching_cubes", _lib.ptr(values), r, ctypes.c_double(fld.dx), ctypes.c_double(iso),
+             ctypes.byref(nv), ctypes.byref(nt))
+    return _fetch_mesh(ctx, nv.value, nt.value)
+
+
+def compute_uvs(mesh: SurfaceMesh, domain_extent) -> SurfaceMesh:
+    """Planar top-down projection (surfacing.py:98-106)."""
+    ext = np.asarray(domain_extent, dtype=np.float64)
+    if len(mesh.vertices):
+        u = np.clip(mesh.vertices[:, 0] / ext[0], 0.0, 1.0)
+        w = np.clip(mesh.vertices[:, 2] / ext[2], 0.0, 1.0)
+        mesh.uvs = np.stack([u, w], axis=1)
+    else:
+        mesh.uvs = np.zeros((0, 2))
+    return mesh
+
+
+def extract_surface(state: SimState, iso: float, resolution=None) -> SurfaceMesh:
+    """splat -> marching cubes -> UVs (surfacing.py:109-112), with the splat
+    and the triangulation on the device: only the mesh is read back."""
+    if iso <= 0.0:
+        raise ParameterError("iso level must be positive")
+    res, dx = _field_geometry(state.grid, resolution)
+    if state.particle_count == 0:
+        return compute_uvs(SurfaceMesh.empty(), state.grid.extent)
+    ctx = _device_state(state)
+    r = (ctypes.c_int32 * 3)(*res)
+    ctx.call("mpm_splat_density", _lib.ptr(None), _lib.ptr(None), ctypes.c_int64(0), r, ctypes.c_double(dx),
+             _lib.ptr(None))
+    nv, nt = ctypes.c_int64(0), ctypes.c_int64(0)
+    ctx.call("mpm_marching_cubes", _lib.ptr(None), _lib.ptr(None, _lib._I32), ctypes.c_double(dx),
+             ctypes.c_double(iso), ctypes.byref(nv), ctypes.byref(nt))
+    return compute_uvs(_fetch_mesh(ctx, nv.value, nt.value), state.grid.extent)
