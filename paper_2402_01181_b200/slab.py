@@ -156,23 +156,30 @@ class LocalExchange:
 
 class TorchExchange:
     """torch.distributed point-to-point between neighbouring ranks (one window
-    per rank): NCCL on CUDA tensors, gloo on CPU tensors."""
+    per rank): NCCL on the device tensors; with the gloo backend (CPU-only
+    point-to-point) the tensors are staged through host memory, which lets
+    the multi-process path run as several processes on one GPU in tests."""
 
-    def __init__(self, window, rank, world, device="cuda"):
+    def __init__(self, window, rank, world, device="cuda", host_staging=None):
+        import torch.distributed as dist
         self.win, self.rank, self.world, self.device = window, rank, world, device
+        self.host_staging = (dist.get_backend() == "gloo") if host_staging is None else bool(host_staging)
 
     def _sendrecv(self, send: dict, recv_shapes: dict, dtype):
         import torch
         import torch.distributed as dist
         ops, out = [], {}
+        where = "cpu" if self.host_staging else self.device
         for nb, t in send.items():
-            ops.append(dist.P2POp(dist.isend, t, nb))
+            ops.append(dist.P2POp(dist.isend, t.to(where) if self.host_staging else t, nb))
         for nb, shape in recv_shapes.items():
-            out[nb] = torch.empty(shape, dtype=dtype, device=t.device if send else self.device)
+            out[nb] = torch.empty(shape, dtype=dtype, device=where)
             ops.append(dist.P2POp(dist.irecv, out[nb], nb))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if self.host_staging:
+            out = {nb: t.to(self.device) for nb, t in out.items()}
         return out
 
     def counts(self, mine: dict):
