@@ -1,3 +1,5 @@
+import sys
+sys.path.insert(0, ".")
 import paper_2402_01181_b200 as sm
 grid = sm.Grid(resolution=(256, 256, 256))
 mats = [sm.Material(1.0e4, 0.3, 1000.0)]
