@@ -346,7 +346,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         prof_ms += frame()
     torch.cuda.synchronize()
-    tbuf = (ctypes.c_double * 14)()
+    tbuf = (ctypes.c_double * 16)()
     L.mpm_get_timing(ctx.h, tbuf)
     L.mpm_set_timing(ctx.h, 0)
     a_ms, a_n = tbuf[0], max(tbuf[1], 1.0)
@@ -354,9 +354,13 @@ def run_ours(args, rank, world, local_rank):
     rebin_ms, g2p_ms = tbuf[4], tbuf[6]
     b_ms, b_n = tbuf[10], max(tbuf[11], 1.0)
     f_ms, f_n = tbuf[12], max(tbuf[13], 1.0)
-    # dominant kernel (largest share of the timed region) for the roofline line
+    m_ms, m_n = tbuf[14], max(tbuf[15], 1.0)
+    # dominant kernel (largest share of the timed region) for the roofline line;
+    # n = launches, or substeps for the cooperative substeps_kernel
     dom, fused_ms, fused_n = max(
-        [("fused_kernel (G2P+advect+F update+stress+P2G, 1 launch = 1 substep)", f_ms, f_n),
+        [("substeps_kernel (cooperative, per substep: fused G2P+advect+F update+stress+P2G phase, "
+          "grid barrier, grid-op phase; time per substep)", m_ms, m_n),
+         ("fused_kernel (G2P+advect+F update+stress+P2G, 1 launch = 1 substep)", f_ms, f_n),
          ("g2p_stress_kernel (G2P+advect+F update+stress, 1 launch = 1 substep)", a_ms, a_n),
          ("p2g_tile_kernel (P2G scatter, 1 launch = 1 substep)", b_ms, b_n)], key=lambda t: t[1])
     t_dev = dev_ms / 1000.0
@@ -429,7 +433,8 @@ def run_ours(args, rank, world, local_rank):
                      "share_of_step": fused_ms / max(prof_ms, 1e-9),
                      "timing": f"mean_launch_ms from a {prof_steps}-frame pass with per-kernel CUDA events "
                                "(value/ms_per_step from the pass without them)"},
-        "kernel_ms": {"fused_mean": f_ms / f_n, "fused_launches": tbuf[13],
+        "kernel_ms": {"substeps_kernel_per_substep": m_ms / m_n, "substeps_kernel_substeps": tbuf[15],
+                      "fused_mean": f_ms / f_n, "fused_launches": tbuf[13],
                       "g2p_stress_mean": a_ms / a_n, "p2g_tile_mean": b_ms / b_n,
                       "grid_op_mean": grid_ms / grid_n,
                       "rebin_total": rebin_ms, "g2p_total": g2p_ms, "device_total": prof_ms,

@@ -17,6 +17,9 @@
 #include "common.cuh"
 #include "mc_table.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace mpm {
 
 #ifdef FUSED_PROFILE
@@ -784,9 +787,12 @@ __device__ __forceinline__ long long fprof_clock_dep(int dep) {
 // Fused steady-state kernel, two barriers per item: [B] after the scatter
 // (tile complete) and [A] after the flush of this item overlapped with the
 // velocity-tile load of the CTA's next item (disjoint shared-memory regions).
-__global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,
-                                                                 float4* __restrict__ bounds_out,
-                                                                 int* __restrict__ item_box) {
+// The fused steady-state substep as a CTA-level phase (used by fused_kernel
+// and, once per substep, by the cooperative substeps_kernel).  zero_tile:
+// the int32 tile is cleared first (the flushes leave it clean afterwards).
+__device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict__ bounds_in,
+                                            float4* __restrict__ bounds_out, int* __restrict__ item_box,
+                                            bool zero_tile) {
   extern __shared__ float smem[];
   float* vtile = smem;                                           // 3 x TILE_NODES
   int* tile = reinterpret_cast<int*>(smem + 3 * TILE_NODES);     // 4 x TILE_NODES
@@ -797,7 +803,8 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   __shared__ float4 nxt_bounds;
   __shared__ int nxt_wi;
   const int nwork = *p.nwork;
-  for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
+  if (zero_tile)
+    for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
   const int rot = threadIdx.x & 3;
   const bool r1 = rot & 1, r2 = rot & 2;
@@ -945,6 +952,12 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   warp_count_add(p.inverted, inverted);
 }
 
+__global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,
+                                                                                  float4* __restrict__ bounds_out,
+                                                                                  int* __restrict__ item_box) {
+  fused_phase(p, bounds_in, bounds_out, item_box, true);
+}
+
 // Final G2P of a frame / stage g2p_advect: thread per particle.
 __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1036,15 +1049,13 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
   return make_float4(v0, v1, v2, a.w);
 }
 
+// The grid op as a CTA-level phase (grid_op_kernel, and once per substep in
+// the cooperative substeps_kernel).
 template <bool DENSE>
-__global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params p, Colliders cs, int clear, int* done) {
+__device__ __forceinline__ void grid_phase(const Params& p, const Colliders& cs, int clear) {
   // one table for the whole grid: the fp32 prefilter boxes are staged in
   // shared memory once per CTA (per-environment tables use collider_near)
   __shared__ ColliderNearF nf_s[MAX_COLLIDERS];
-#ifdef FUSED_PROFILE
-  unsigned long long g_t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
-#endif
   const bool staged = !cs.per_env && cs.theta >= 0.0 && cs.count > 0 && cs.count <= MAX_COLLIDERS;
   if (staged && threadIdx.x < cs.count) nf_s[threadIdx.x] = make_near_f(cs, threadIdx.x, cs.theta_f);
   __syncthreads();
@@ -1104,6 +1115,15 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
       a11 = a21;
     }
   }
+}
+
+template <bool DENSE>
+__global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params p, Colliders cs, int clear, int* done) {
+#ifdef FUSED_PROFILE
+  unsigned long long g_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
+#endif
+  grid_phase<DENSE>(p, cs, clear);
 #ifdef FUSED_PROFILE
   {
     __syncthreads();
@@ -1135,6 +1155,44 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
         __threadfence();
       }
     }
+  }
+}
+
+// Substeps 2..L of a stretch in ONE cooperative launch: per substep the
+// fused phase (all items) and the grid-op phase (all active bricks),
+// separated by grid-wide barriers, so the kernel boundaries (launch, ramp,
+// tail, the grid op's fixed per-launch work) of two launches per substep
+// disappear.  Brick-list and work-item counters are double-buffered by
+// substep parity (ctr[0..1] active bricks, ctr[2..3] work cursor; both of the
+// first pair zero at launch): substep t uses parity t & 1 and CTA 0 re-arms
+// parity t + 1, whose last users finished before the previous barrier.  The
+// item bounds swap per substep exactly as across fused_kernel launches.
+// Collider pose rows: row0 + t, clamped to the table.
+__global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS)
+    substeps_kernel(Params p, Colliders cs, const ColliderPose* __restrict__ pose_base, int pose_rows,
+                    int pose_stride, int row0, int nsub, int last_clear, float4* __restrict__ bounds_in,
+                    float4* __restrict__ bounds_out, int* __restrict__ item_box, int* __restrict__ ctr,
+                    int* __restrict__ final_active) {
+  cg::grid_group grid = cg::this_grid();
+  for (int t = 0; t < nsub; ++t) {
+    Params q = p;
+    q.active_count = ctr + (t & 1);
+    q.work_next = ctr + 2 + (t & 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctr[(t + 1) & 1] = 0;
+      ctr[2 + ((t + 1) & 1)] = 0;
+    }
+    fused_phase(q, bounds_in, bounds_out, item_box, t == 0);
+    float4* tmp = bounds_in;
+    bounds_in = bounds_out;
+    bounds_out = tmp;
+    grid.sync();
+    Colliders c = cs;
+    if (pose_base) c.pose = pose_base + (long long)min(row0 + t, pose_rows - 1) * pose_stride;
+    const int clear = t < nsub - 1 || last_clear;
+    grid_phase<false>(q, c, clear);
+    if (t == nsub - 1 && !clear && blockIdx.x == 0 && threadIdx.x == 0) *final_active = *q.active_count;
+    grid.sync();
   }
 }
 

@@ -133,7 +133,7 @@ struct mpm_ctx {
 
   // optional per-kernel timing: event pairs per launch, resolved lazily
   bool timing = false;
-  struct Mark { int kind; cudaEvent_t a, b; bool graph_owned; };
+  struct Mark { int kind; cudaEvent_t a, b; bool graph_owned; int weight; };
   std::vector<Mark> marks;
 
   // CUDA graphs of whole fast-path frames, keyed by the host-side start state
@@ -151,9 +151,12 @@ struct mpm_ctx {
   bool graphs_on = true;
   float4* bounds_a = nullptr;  // the two item-bound arrays as allocated (swap parity)
   std::vector<cudaEvent_t> event_pool;
-  double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
   int items_per_sm = 4;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
+  bool mega_on = false;   // substeps 2..L as one cooperative substeps_kernel (option "mega" / SOFTMPM_MEGA=1)
+  int mega_blocks = 0;
+  bool mega_coop = false;  // device supports cooperative launches
   bool counters_clean = true;     // counters[0] (active bricks) and [3] (work_next) known zero
   bool bounds_out_clean = false;  // item_bounds2 known zero
 };
@@ -219,8 +222,9 @@ cudaEvent_t pool_event(mpm_ctx* ctx) {
 struct TimedRegion {
   mpm_ctx* ctx;
   int kind;
+  int weight;  // launches this region stands for (substeps_kernel: its substeps)
   cudaEvent_t a = nullptr;
-  TimedRegion(mpm_ctx* c, int k) : ctx(c), kind(k) {
+  TimedRegion(mpm_ctx* c, int k, int w = 1) : ctx(c), kind(k), weight(w) {
     if (ctx->timing) {
       a = pool_event(ctx);
       record(a);
@@ -230,7 +234,7 @@ struct TimedRegion {
     if (a) {
       cudaEvent_t b = pool_event(ctx);
       record(b);
-      ctx->marks.push_back({kind, a, b, false});
+      ctx->marks.push_back({kind, a, b, false, weight});
     }
   }
   // inside stream capture a plain record is only a dependency marker: timing
@@ -252,7 +256,7 @@ void resolve_marks(mpm_ctx* ctx) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, mk.a, mk.b);
     ctx->acc[2 * mk.kind] += ms;
-    ctx->acc[2 * mk.kind + 1] += 1.0;
+    ctx->acc[2 * mk.kind + 1] += mk.weight;
     if (!mk.graph_owned) {
       ctx->event_pool.push_back(mk.a);
       ctx->event_pool.push_back(mk.b);
@@ -550,6 +554,45 @@ int launch_grid_op(mpm_ctx* ctx, bool dense, bool use_col, int row, bool clear) 
   return 0;
 }
 
+// Substeps row0 .. row0 + nsub - 1 (after the first of a stretch) as one
+// cooperative substeps_kernel launch.
+int launch_substeps(mpm_ctx* ctx, bool use_col, int row0, int nsub, bool last_clear) {
+  Params p = make_params(ctx);
+  Colliders cs = make_colliders(ctx, row0, use_col);
+  int* ctr = ctx->counters + 50;  // [50..51] active bricks, [52..53] work cursor (by substep parity)
+  CK(cudaMemsetAsync(ctr, 0, 4 * sizeof(int), ctx->stream));
+  if (!ctx->bounds_out_clean)
+    CK(cudaMemsetAsync(ctx->item_bounds2, 0, sizeof(float4) * ctx->work_cap, ctx->stream));
+  const ColliderPose* pose_base = ctx->pose;
+  int pose_rows = std::max(ctx->pose_rows, 1);
+  int pose_stride = std::max(ctx->ncol, 1);
+  int lc = last_clear ? 1 : 0;
+  float4* bin = ctx->item_bounds;
+  float4* bout = ctx->item_bounds2;
+  int* final_active = ctx->counters;
+  void* args[] = {&p, &cs, &pose_base, &pose_rows, &pose_stride, &row0, &nsub, &lc, &bin, &bout,
+                  &ctx->item_box, &ctr, &final_active};
+  cudaLaunchConfig_t lc_cfg = {};
+  lc_cfg.gridDim = dim3(ctx->mega_blocks);
+  lc_cfg.blockDim = dim3(FUSED_K_THREADS);
+  lc_cfg.dynamicSmemBytes = sizeof(float) * 7 * TILE_NODES;
+  lc_cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc_cfg.attrs = attr;
+  lc_cfg.numAttrs = 1;
+  {
+    TimedRegion tr(ctx, 6, nsub);
+    CK(cudaLaunchKernelExC(&lc_cfg, (const void*)substeps_kernel, args));
+    LAUNCHED();
+  }
+  if (nsub & 1) std::swap(ctx->item_bounds, ctx->item_bounds2);
+  ctx->bounds_out_clean = true;
+  ctx->counters_clean = false;
+  return 0;
+}
+
 int launch_g2p(mpm_ctx* ctx) {
   TimedRegion tr(ctx, 3);
   Params p = make_params(ctx);
@@ -613,9 +656,15 @@ int run_fast_sequence(mpm_ctx* ctx, int nsub, bool col) {
   while (s < nsub) {
     const int L = std::min(ctx->cfg.rebin_interval, nsub - s);
     TRY(rebin(ctx));
-    for (int t = 0; t < L; ++t) {
-      TRY(launch_fused(ctx, t > 0));
-      TRY(launch_grid_op(ctx, false, col, s + t, s + t != nsub - 1));
+    if (ctx->mega_on && L > 1) {
+      TRY(launch_fused(ctx, false));
+      TRY(launch_grid_op(ctx, false, col, s, s != nsub - 1));
+      TRY(launch_substeps(ctx, col, s + 1, L - 1, s + L - 1 != nsub - 1));
+    } else {
+      for (int t = 0; t < L; ++t) {
+        TRY(launch_fused(ctx, t > 0));
+        TRY(launch_grid_op(ctx, false, col, s + t, s + t != nsub - 1));
+      }
     }
     TRY(launch_g2p(ctx));
     s += L;
@@ -702,6 +751,16 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
     ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
     ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES);
+    cudaFuncSetAttribute(substeps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * 7 * TILE_NODES));
+    ctx->mega_blocks = persistent((const void*)substeps_kernel, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES);
+    {
+      int coop = 0;
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->dev);
+      const char* mg = getenv("SOFTMPM_MEGA");
+      ctx->mega_coop = coop != 0;
+      ctx->mega_on = coop && mg && mg[0] == '1';
+    }
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   }
   if (rc) {
@@ -1197,6 +1256,10 @@ int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
   } else if (!strcmp(key, "split")) {
     invalidate_graphs(ctx);
     ctx->split_mode = value != 0;
+  } else if (!strcmp(key, "mega")) {
+    if (value && !ctx->mega_coop) return fail(ctx, MPM_EINVAL, "mega: device has no cooperative launch");
+    invalidate_graphs(ctx);
+    ctx->mega_on = value != 0;
   } else {
     return fail(ctx, MPM_EINVAL, std::string("unknown option ") + key);
   }
@@ -1454,6 +1517,8 @@ int mpm_get_timing(mpm_ctx* ctx, double* out) {
   out[11] = ctx->acc[9];
   out[12] = ctx->acc[10];
   out[13] = ctx->acc[11];
+  out[14] = ctx->acc[12];
+  out[15] = ctx->acc[13];
   for (double& a : ctx->acc) a = 0.0;
   return 0;
 }

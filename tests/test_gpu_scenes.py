@@ -208,3 +208,19 @@ def _traj_c4():
     return [sm.Keyframe(0.0, [(np.array([0.5, y0, 0.5]), q)]),
             sm.Keyframe(0.05, [(np.array([0.5, y0 - 0.025, 0.5]), q)]),
             sm.Keyframe(10.0, [(np.array([0.5, y0 - 0.025, 0.5]), q)])]
+
+
+def test_cooperative_substeps_kernel_matches_per_substep_launches():
+    """Option "mega": substeps 2..L as one cooperative launch (fused phase,
+    grid barrier, grid-op phase) reproduces the per-substep launches."""
+    res = {}
+    for mega in (0, 1):
+        st, mats, params, cols, pose_fn = scenes.c2()
+        params.rebin_interval = 10
+        sm.step(st, mats, params, cols, pose_fn)  # creates the context
+        st._ctx.call("mpm_set_option", b"mega", mega)
+        for _ in range(4):
+            sm.step(st, mats, params, cols, pose_fn)
+        res[mega] = (st.x.copy(), st.v.copy(), st.F.copy())
+    for a, b in zip(res[0], res[1]):
+        assert rel_l2(a, b) < 1e-5
