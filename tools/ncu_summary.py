@@ -34,11 +34,14 @@ def full(rep):
                   if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued") and _f(v) is not None}
         tot = sum(stalls.values()) or 1.0
         rd, wr = _f(d.get("dram__bytes_read.sum")), _f(d.get("dram__bytes_write.sum"))
-        unit_r = hdr and rows[1][hdr.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in hdr else ""
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1e6)
+        units = dict(zip(hdr, rows[1]))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units.get("dram__bytes_read.sum", ""), 1e6)
+        tscale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6}.get(
+            units.get("gpu__time_duration.sum", ""), 1.0)
+        dur = _f(d.get("gpu__time_duration.sum"))
         rec = {
             "kernel": d.get("Kernel Name"),
-            "duration_us": _f(d.get("gpu__time_duration.sum")),
+            "duration_us": dur * tscale if dur is not None else None,
             "dram_read_bytes": rd * scale if rd is not None else None,
             "dram_write_bytes": wr * scale if wr is not None else None,
             "issue_active_pct": _f(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")),
