@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
 // in one pass per work item, with no payload round trip (the per-substep
 // working set x, F, m, V0 + grid stays L2-resident).  The G2P reads the
 // shared-memory velocity tile of the node box the item scattered to in the
-// previous substep; the P2G scatters lane-rotated channels into the int32
+// previous substep; the P2G scatters cell-rank-rotated channels into the int32
 // fixed-point tile whose scales come from the item's bounds in the previous
 // substep (x BOUND_SAFETY for momentum, exact for mass).  A particle that
 // exceeds those bounds or leaves the tile is scattered with float REDG.F32x4
@@ -806,11 +806,6 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
   if (zero_tile)
     for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
-  const int rot = threadIdx.x & 3;
-  const bool r1 = rot & 1, r2 = rot & 2;
-  int off[4];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) off[s] = ((s + rot) & 3) * TILE_NODES;
   unsigned inverted = 0;
   int par = 0;
   // dynamic scheduling over the size-sorted work list: the first gridDim.x
@@ -849,9 +844,6 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
     // previous item's box buffer (its flush ended before the last [A])
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
     const float S[4] = {scale_s[par][0], scale_s[par][1], scale_s[par][2], scale_s[par][3]};
-    float sc[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) sc[s] = sel4(r1, r2, S[s & 3], S[(s + 1) & 3], S[(s + 2) & 3], S[(s + 3) & 3]);
     float mx[4] = {0.f, 0.f, 0.f, 0.f};
     int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
@@ -892,7 +884,23 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
         lo_c[a] = min(lo_c[a], lc[a]);
         hi_c[a] = max(hi_c[a], lc[a]);
       }
-      tile_scatter_rot(tile, off, r1, r2, sc, q, lc, p.dx);
+      {
+        // rotate the channel order by the particle's rank among this round's
+        // lanes in the same base cell: the first particle of every cell
+        // writes channel s at step s, so different cells of a warp row spread
+        // over consecutive banks and same-cell lanes over channel planes
+        const unsigned grp = __match_any_sync(__activemask(), (lc[0] * TILE + lc[1]) * TILE + lc[2]);
+        const int crot = __popc(grp & ((1u << (threadIdx.x & 31)) - 1u)) & 3;
+        const bool c1 = crot & 1, c2 = crot & 2;
+        int coff[4];
+        float csc[4];
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          coff[s2] = ((s2 + crot) & 3) * TILE_NODES;
+          csc[s2] = sel4(c1, c2, S[s2 & 3], S[(s2 + 1) & 3], S[(s2 + 2) & 3], S[(s2 + 3) & 3]);
+        }
+        tile_scatter_rot(tile, coff, c1, c2, csc, q, lc, p.dx);
+      }
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
