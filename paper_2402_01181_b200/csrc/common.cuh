@@ -32,7 +32,16 @@ constexpr int MARGIN = MPM_MARGIN;        // tile margin for particles drifting 
 // nodes per tile edge (14): base cells org + [0, TILE - 3], i.e. drift of
 // MARGIN - 1 cells below the bin and TILE - BIN - 1 - MARGIN above
 constexpr int TILE = MPM_TILE;
-constexpr int TILE_NODES = TILE * TILE * TILE;
+#ifndef MPM_TILE_ZSTRIDE
+#define MPM_TILE_ZSTRIDE TILE
+#endif
+#ifndef MPM_PLANE_PAD
+#define MPM_PLANE_PAD 0
+#endif
+// smem tile layout: node (x, y, z) at (x TILE + y) TILE_Z + z of a channel
+// plane of TILE_NODES words (z stride and plane padding tune the bank map)
+constexpr int TILE_Z = MPM_TILE_ZSTRIDE;
+constexpr int TILE_NODES = TILE * TILE * TILE_Z + MPM_PLANE_PAD;
 constexpr int FUSED_THREADS = 256;      // stage A (g2p_stress_kernel)
 #ifndef MPM_FUSED_THREADS
 #define MPM_FUSED_THREADS 256

@@ -98,8 +98,8 @@ struct TileVel {
   __device__ __forceinline__ void offsets(const int b[3], int ox[3], int oy[3], int oz[3]) const {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      ox[q] = (b[0] - org[0] + q) * TILE * TILE;
-      oy[q] = (b[1] - org[1] + q) * TILE;
+      ox[q] = (b[0] - org[0] + q) * TILE * TILE_Z;
+      oy[q] = (b[1] - org[1] + q) * TILE_Z;
       oz[q] = (b[2] - org[2] + q);
     }
   }
@@ -243,8 +243,8 @@ __device__ __forceinline__ void p2g_scatter(const Params& p, int* tile, const in
   if (TILE_MODE) {
 #pragma unroll
     for (int o = 0; o < 3; ++o) {
-      ox[o] = (q.b[0] - org[0] + o) * TILE * TILE;
-      oy[o] = (q.b[1] - org[1] + o) * TILE;
+      ox[o] = (q.b[0] - org[0] + o) * TILE * TILE_Z;
+      oy[o] = (q.b[1] - org[1] + o) * TILE_Z;
       oz[o] = (q.b[2] - org[2] + o);
     }
   } else {
@@ -399,7 +399,7 @@ __device__ __forceinline__ void load_vtile_column(const Params& p, float* vtile,
 #pragma unroll
     for (int u = 0; u < G; ++u) {
       if (xs + u <= x1) {
-        const int t = ((xs + u) * TILE + ty) * TILE + tz;
+        const int t = ((xs + u) * TILE + ty) * TILE_Z + tz;
         vtile[t] = g[u].x;
         vtile[TILE_NODES + t] = g[u].y;
         vtile[2 * TILE_NODES + t] = g[u].z;
@@ -422,7 +422,7 @@ __device__ __forceinline__ void load_vtile_column_async(const Params& p, float* 
   for (int tx = x0; tx <= x1; ++tx) {
     const int gi = orgx + tx;
     const float* src = reinterpret_cast<const float*>(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
-    const int t = (tx * TILE + ty) * TILE + tz;
+    const int t = (tx * TILE + ty) * TILE_Z + tz;
     cp_async4(vtile + t, src);
     cp_async4(vtile + TILE_NODES + t, src + 1);
     cp_async4(vtile + 2 * TILE_NODES + t, src + 2);
@@ -538,7 +538,7 @@ __device__ __forceinline__ void tile_scatter_rot(int* tile, const int off[4], bo
 #pragma unroll
     for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * dx;
   }
-  const int base = (lc[0] * TILE + lc[1]) * TILE + lc[2];
+  const int base = (lc[0] * TILE + lc[1]) * TILE_Z + lc[2];
 #pragma unroll
   for (int ii = 0; ii < 3; ++ii) {
 #pragma unroll
@@ -550,7 +550,7 @@ __device__ __forceinline__ void tile_scatter_rot(int* tile, const int off[4], bo
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float wt = wij * w[2][k];
-        int* t = tile + base + (ii * TILE + j) * TILE + k;
+        int* t = tile + base + (ii * TILE + j) * TILE_Z + k;
 #pragma unroll
         for (int s = 0; s < 4; ++s) atomicAdd(t + off[s], fixq(wt, bij[s] + as[s][2] * dxs[2][k]));
       }
@@ -584,14 +584,14 @@ __device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int
     int4 a[SEG];
 #pragma unroll
     for (int k = 0; k < SEG; ++k) {
-      const int t = ((xs + k) * TILE + ty) * TILE + tz;
+      const int t = ((xs + k) * TILE + ty) * TILE_Z + tz;
       a[k] = xs + k <= x1 ? make_int4(tile[t], tile[TILE_NODES + t], tile[2 * TILE_NODES + t], tile[3 * TILE_NODES + t])
                           : make_int4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int k = 0; k < SEG; ++k) {
       if (xs + k > x1) continue;
-      const int t = ((xs + k) * TILE + ty) * TILE + tz;
+      const int t = ((xs + k) * TILE + ty) * TILE_Z + tz;
       tile[t] = 0;
       tile[TILE_NODES + t] = 0;
       tile[2 * TILE_NODES + t] = 0;
