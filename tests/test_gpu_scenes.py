@@ -224,3 +224,25 @@ def test_cooperative_substeps_kernel_matches_per_substep_launches():
         res[mega] = (st.x.copy(), st.v.copy(), st.F.copy())
     for a, b in zip(res[0], res[1]):
         assert rel_l2(a, b) < 1e-5
+
+
+def test_two_materials_match_oracle():
+    """Per-particle material ids (SimParams materials list, materials.py:77-82):
+    a stiff and a soft block side by side on the floor, 2 frames, against the
+    O1 oracle with the same per-material (mu, lam)."""
+    grid = sm.Grid((48, 48, 48))
+    mats = [sm.Material(2.0e4, 0.3, 1000.0), sm.Material(3.0e3, 0.45, 1100.0)]
+    a = sm.sample_box((0.35, 0.16, 0.5), (0.2, 0.15, 0.25), 6000, seed=1, grid=grid)
+    b = sm.ParticleSpawn(sm.sample_box((0.65, 0.16, 0.5), (0.2, 0.15, 0.25), 6000, seed=2, grid=grid).positions,
+                         a.rest_volume_per_particle, 1)
+    st = sm.SimState.from_spawns(grid, [a, b], mats)
+    assert set(np.unique(st.material_id)) == {0, 1}
+    params = sm.SimParams()
+    osim = O.OracleSim(O.OracleParams(res=grid.resolution, dx=grid.dx), st.x, st.v, st.F, st.C, st.mass, st.vol0,
+                       st.material_id, [m.mu for m in mats], [m.lam for m in mats])
+    for _ in range(2):
+        sm.step(st, mats, params)
+        for _ in range(params.substeps_per_frame):
+            osim.substep(None)
+    for k in ("x", "v", "F"):
+        assert rel_l2(getattr(st, k), getattr(osim, k)) < 1e-4, k
