@@ -470,7 +470,10 @@ def run_slab(args, rank, world, local_rank):
                             ghost_bricks=2, device=local_rank)
     win = wins[rank]
     del wins, st, x, v, F, C
-    ex = slab.TorchExchange(win, rank, world, device=f"cuda:{local_rank}")
+    if args.exchange == "ipc":
+        ex = slab.IpcExchange(win, rank, world, device=f"cuda:{local_rank}")
+    else:
+        ex = slab.TorchExchange(win, rank, world, device=f"cuda:{local_rank}")
     for _ in range(args.warmup):
         slab.step_distributed(win, ex, mats, params)
     n_local = int(_lib_count(win))
@@ -490,7 +493,8 @@ def run_slab(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
             "config": {"workload": f"c5: {int(n_total)} particles, {g.resolution[0]}^3 grid, x-slabs over "
-                                   f"{world} GPUs (NCCL halo + migration; wall clock incl. exchanges)",
+                                   f"{world} GPUs ({'peer-memory (IPC/NVLink) halo' if args.exchange == 'ipc' else 'NCCL halo'}"
+                                   f" + NCCL migration; wall clock incl. exchanges)",
                        "parallelism": f"slab x{world}"},
         }), flush=True)
 
@@ -510,6 +514,9 @@ def main():
     ap.add_argument("--envs", type=int, default=1024, help="c4: environments over all ranks")
     ap.add_argument("--rebin", type=int, default=None, help="override SimParams.rebin_interval")
     ap.add_argument("--particles", type=int, default=None)
+    ap.add_argument("--exchange", default="ipc", choices=["ipc", "nccl"],
+                    help="c5 over ranks: halo through peer memory (pack kernels write into the neighbour's "
+                         "IPC-mapped buffers) or NCCL send/recv")
     ap.add_argument("--cpu-substeps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -128,6 +128,22 @@ int mpm_g2p(mpm_ctx *ctx);
 int mpm_substeps(mpm_ctx *ctx, int nsub, int use_colliders, int64_t *inverted,
                  double *device_ms);
 
+/* Peer-memory halo exchange (NVLink P2P / CUDA IPC), the device-side
+ * alternative to mpm_halo_pack / unpack_* + a host transport.  Per side the
+ * context exports its receive buffers and two interprocess events as an
+ * mpm_ipc_blob_size() byte blob (mpm_ipc_export) that the neighbour maps
+ * (mpm_ipc_import with its opposite side).  mpm_ipc_halo(phase, sides):
+ * 0 packs our ghost momentum straight into each neighbour's buffers, 1 adds
+ * what the neighbours wrote into ours, 2 writes the velocities of those
+ * bricks back into the neighbours, 3 applies the velocities we received; all
+ * stream-ordered with event waits, counts stay on the device.  The caller
+ * orders each phase pair (0 before the neighbours' 1, 2 before their 3) with
+ * a host barrier, so that every event wait follows the record it needs. */
+int64_t mpm_ipc_blob_size(void);
+int mpm_ipc_export(mpm_ctx *ctx, int side, void *blob);
+int mpm_ipc_import(mpm_ctx *ctx, int side, const void *peer_blob);
+int mpm_ipc_halo(mpm_ctx *ctx, int phase, int sides);
+
 /* ---- slab decomposition (BASELINE config 5) ------------------------------
  * A context can own an x-window of a larger global grid: its res[0] nodes
  * start at global node offset[0] (multiple of 4) and include `ghost_bricks`

@@ -1945,6 +1945,84 @@ __global__ void halo_unpack_vel_kernel(Params p, const int* rec_ids, const float
   }
 }
 
+// ---- peer-memory halo exchange (CUDA IPC / NVLink P2P) ------------------
+// The pack kernels write straight into the NEIGHBOUR's receive buffers
+// (mapped with cudaIpcOpenMemHandle; P2P stores and atomics over NVLink
+// between GPUs), so packing and the transfer are one kernel; record counts
+// live on the device and never visit the host.
+
+// Ghost bricks of one side -> the neighbour's receive buffers; slot from the
+// neighbour's counter, the global ids also kept locally for the velocity reply.
+__global__ void ipc_pack_kernel(Params p, int side, int gb, int* peer_ids, float4* peer_data, int* peer_count,
+                                int* my_ids, int* my_sent) {
+  const int nitems = *p.active_count;
+  const int lane = threadIdx.x & 31;
+  for (int it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems;
+       it += gridDim.x * (blockDim.x >> 5)) {
+    const int b = p.active_list[it];
+    const int bi = b / (p.nb[1] * p.nb[2]);
+    const bool ghost = side == 0 ? bi < gb : bi >= p.nb[0] - gb;
+    if (!ghost) continue;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(peer_count, 1);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (lane == 0) {
+      const int rem = b - bi * (p.nb[1] * p.nb[2]);
+      const int gbid = (bi + (p.goff[0] >> BRICK_SHIFT)) * (p.nb[1] * p.nb[2]) + rem;
+      peer_ids[slot] = gbid;
+      my_ids[slot] = gbid;
+      atomicMax(my_sent, slot + 1);
+    }
+    peer_data[(long long)slot * 64 + lane] = p.gm[((long long)b << 6) + lane];
+    peer_data[(long long)slot * 64 + lane + 32] = p.gm[((long long)b << 6) + lane + 32];
+  }
+}
+
+__global__ void ipc_unpack_add_kernel(Params p, const int* rec_ids, const float4* rec_data, const int* count,
+                                      int* local_ids) {
+  const int n = *count;
+  const int lane = threadIdx.x & 31;
+  const int per_slab = p.nb[1] * p.nb[2];
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
+    const int b = rec_ids[r] - (p.goff[0] >> BRICK_SHIFT) * per_slab;
+    if (lane == 0) local_ids[r] = b;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long idx = ((long long)b << 6) + lane + 32 * h;
+      const float4 a = rec_data[(long long)r * 64 + lane + 32 * h];
+      float4 g = p.gm[idx];
+      g.x += a.x;
+      g.y += a.y;
+      g.z += a.z;
+      g.w += a.w;
+      p.gm[idx] = g;
+    }
+    if (lane == 0) mark_brick(p, (long long)b << 6);
+  }
+}
+
+// Velocity reply straight into the neighbour's velocity receive buffer.
+__global__ void ipc_pack_vel_kernel(Params p, const int* local_ids, const int* n_recv, float4* peer_vdata) {
+  const int n = *n_recv;
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
+    const long long b = local_ids[r];
+    peer_vdata[(long long)r * 64 + lane] = p.gv[(b << 6) + lane];
+    peer_vdata[(long long)r * 64 + lane + 32] = p.gv[(b << 6) + lane + 32];
+  }
+}
+
+__global__ void ipc_unpack_vel_kernel(Params p, const int* my_ids, const int* my_sent, const float4* vdata) {
+  const int n = *my_sent;
+  const int lane = threadIdx.x & 31;
+  const int per_slab = p.nb[1] * p.nb[2];
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
+    const long long b = my_ids[r] - (p.goff[0] >> BRICK_SHIFT) * per_slab;
+    p.gv[(b << 6) + lane] = vdata[(long long)r * 64 + lane];
+    p.gv[(b << 6) + lane + 32] = vdata[(long long)r * 64 + lane + 32];
+  }
+}
+
 // Migration: flag = 0 keep, 1 leaves to the low neighbour, 2 to the high one
 // (global base cell x outside [own_lo, own_hi)).
 __global__ void migrant_flag_kernel(Params p, int own_lo, int own_hi, int* flag) {

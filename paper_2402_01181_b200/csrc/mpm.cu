@@ -123,6 +123,17 @@ struct mpm_ctx {
   int* h_local_ids[2] = {nullptr, nullptr};
   int h_recv_n[2] = {0, 0};
   long long h_cap = 0;  // records per buffer
+  // peer-memory exchange (mpm_ipc_*): per side our velocity receive buffer,
+  // counters {recv count, received last, sent}, events, and the neighbour's
+  // mapped buffers / events
+  float4* ipc_vrecv[2] = {nullptr, nullptr};
+  int* ipc_cnt[2] = {nullptr, nullptr};
+  cudaEvent_t ipc_free[2] = {nullptr, nullptr}, ipc_ready[2] = {nullptr, nullptr};
+  int* peer_ids[2] = {nullptr, nullptr};
+  float4* peer_data[2] = {nullptr, nullptr};
+  int* peer_cnt[2] = {nullptr, nullptr};
+  float4* peer_vdata[2] = {nullptr, nullptr};
+  cudaEvent_t peer_free[2] = {nullptr, nullptr}, peer_ready[2] = {nullptr, nullptr};
   int stage_nsub = 0, stage_col = 0;
   // migration scratch
   int* mflag = nullptr;
@@ -795,6 +806,14 @@ int mpm_destroy(mpm_ctx* ctx) {
   }
 #endif
   invalidate_graphs(ctx);
+  for (int sd = 0; sd < 2; ++sd) {
+    for (void* q : {(void*)ctx->peer_ids[sd], (void*)ctx->peer_data[sd], (void*)ctx->peer_cnt[sd], (void*)ctx->peer_vdata[sd]})
+      if (q) cudaIpcCloseMemHandle(q);
+    for (cudaEvent_t e : {ctx->ipc_free[sd], ctx->ipc_ready[sd], ctx->peer_free[sd], ctx->peer_ready[sd]})
+      if (e) cudaEventDestroy(e);
+    if (ctx->ipc_vrecv[sd]) cudaFree(ctx->ipc_vrecv[sd]);
+    if (ctx->ipc_cnt[sd]) cudaFree(ctx->ipc_cnt[sd]);
+  }
   void* bufs[] = {ctx->gm, ctx->gv, ctx->brick_flag, ctx->active_list, ctx->counters, ctx->P[0], ctx->P[1], ctx->item_bounds, ctx->item_bounds2, ctx->pay, ctx->lcell, ctx->sidx, ctx->slc, ctx->bperm, ctx->item_box, ctx->mflag, ctx->mig_rows[0], ctx->mig_rows[1], ctx->h_send_ids[0], ctx->h_send_ids[1],
                   ctx->h_send_data[0], ctx->h_send_data[1], ctx->h_recv_ids[0], ctx->h_recv_ids[1], ctx->h_recv_data[0],
                   ctx->h_recv_data[1], ctx->h_local_ids[0], ctx->h_local_ids[1],
@@ -1551,6 +1570,103 @@ int mpm_set_slab(mpm_ctx* ctx, const int* global_res, const int* offset, int gho
       TRY(dalloc(ctx, &ctx->h_local_ids[s], (size_t)cap));
     }
     ctx->h_cap = cap;
+  }
+  return 0;
+}
+
+// ---- peer-memory halo exchange --------------------------------------------
+constexpr size_t IPC_BLOB = 4 * sizeof(cudaIpcMemHandle_t) + 2 * sizeof(cudaIpcEventHandle_t);
+
+int mpm_ipc_export(mpm_ctx* ctx, int side, void* out) {
+  if (!ctx || side < 0 || side > 1 || !out) return MPM_EINVAL;
+  if (!ctx->h_cap) return fail(ctx, MPM_ESTATE, "ipc_export: call mpm_set_slab first");
+  CK(cudaSetDevice(ctx->dev));
+  if (!ctx->ipc_vrecv[side]) {
+    TRY(dalloc(ctx, &ctx->ipc_vrecv[side], (size_t)(ctx->h_cap + 1) * 64));
+    TRY(dalloc(ctx, &ctx->ipc_cnt[side], 4));
+    CK(cudaMemset(ctx->ipc_cnt[side], 0, 4 * sizeof(int)));
+    CK(cudaEventCreateWithFlags(&ctx->ipc_free[side], cudaEventInterprocess | cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ipc_ready[side], cudaEventInterprocess | cudaEventDisableTiming));
+  }
+  char* o = static_cast<char*>(out);
+  cudaIpcMemHandle_t mh;
+  void* mems[4] = {ctx->h_recv_ids[side], ctx->h_recv_data[side], ctx->ipc_cnt[side], ctx->ipc_vrecv[side]};
+  for (int k = 0; k < 4; ++k) {
+    CK(cudaIpcGetMemHandle(&mh, mems[k]));
+    memcpy(o + k * sizeof(mh), &mh, sizeof(mh));
+  }
+  cudaIpcEventHandle_t eh;
+  CK(cudaIpcGetEventHandle(&eh, ctx->ipc_free[side]));
+  memcpy(o + 4 * sizeof(mh), &eh, sizeof(eh));
+  CK(cudaIpcGetEventHandle(&eh, ctx->ipc_ready[side]));
+  memcpy(o + 4 * sizeof(mh) + sizeof(eh), &eh, sizeof(eh));
+  return 0;
+}
+
+int mpm_ipc_import(mpm_ctx* ctx, int side, const void* peer) {
+  if (!ctx || side < 0 || side > 1 || !peer) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const char* o = static_cast<const char*>(peer);
+  cudaIpcMemHandle_t mh[4];
+  for (int k = 0; k < 4; ++k) memcpy(&mh[k], o + k * sizeof(cudaIpcMemHandle_t), sizeof(cudaIpcMemHandle_t));
+  void* q[4];
+  for (int k = 0; k < 4; ++k) CK(cudaIpcOpenMemHandle(&q[k], mh[k], cudaIpcMemLazyEnablePeerAccess));
+  ctx->peer_ids[side] = static_cast<int*>(q[0]);
+  ctx->peer_data[side] = static_cast<float4*>(q[1]);
+  ctx->peer_cnt[side] = static_cast<int*>(q[2]);
+  ctx->peer_vdata[side] = static_cast<float4*>(q[3]);
+  cudaIpcEventHandle_t eh[2];
+  memcpy(&eh[0], o + 4 * sizeof(cudaIpcMemHandle_t), sizeof(cudaIpcEventHandle_t));
+  memcpy(&eh[1], o + 4 * sizeof(cudaIpcMemHandle_t) + sizeof(cudaIpcEventHandle_t), sizeof(cudaIpcEventHandle_t));
+  CK(cudaIpcOpenEventHandle(&ctx->peer_free[side], eh[0]));
+  CK(cudaIpcOpenEventHandle(&ctx->peer_ready[side], eh[1]));
+  return 0;
+}
+
+int64_t mpm_ipc_blob_size(void) { return (int64_t)IPC_BLOB; }
+
+int mpm_ipc_halo(mpm_ctx* ctx, int phase, int sides) {
+  if (!ctx || phase < 0 || phase > 3) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  Params p = make_params(ctx);
+  for (int sd = 0; sd < 2; ++sd) {
+    if (!((sides >> sd) & 1)) continue;
+    if (!ctx->peer_ids[sd] || !ctx->ipc_cnt[sd]) return fail(ctx, MPM_ESTATE, "ipc_halo: side not connected");
+    int* cnt = ctx->ipc_cnt[sd];  // [0] records received, [1] received last, [2] records sent
+    switch (phase) {
+      case 0:  // ghost momentum -> neighbour (after it consumed our last writes)
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_free[sd], 0));
+        ipc_pack_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, sd, ctx->ghost_bricks, ctx->peer_ids[sd],
+                                                               ctx->peer_data[sd], ctx->peer_cnt[sd],
+                                                               ctx->h_send_ids[sd], cnt + 2);
+        LAUNCHED();
+        CK(cudaEventRecord(ctx->ipc_ready[sd], ctx->stream));
+        break;
+      case 1:  // add the neighbour's ghost momentum into our owned bricks
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_ready[sd], 0));
+        ipc_unpack_add_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_recv_ids[sd], ctx->h_recv_data[sd], cnt,
+                                                                     ctx->h_local_ids[sd]);
+        LAUNCHED();
+        CK(cudaMemcpyAsync(cnt + 1, cnt, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemsetAsync(cnt, 0, sizeof(int), ctx->stream));
+        CK(cudaEventRecord(ctx->ipc_free[sd], ctx->stream));
+        break;
+      case 2:  // velocities of the received bricks -> neighbour
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_free[sd], 0));
+        ipc_pack_vel_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_local_ids[sd], cnt + 1,
+                                                                   ctx->peer_vdata[sd]);
+        LAUNCHED();
+        CK(cudaEventRecord(ctx->ipc_ready[sd], ctx->stream));
+        break;
+      case 3:  // the owner's velocities into our ghost bricks
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_ready[sd], 0));
+        ipc_unpack_vel_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_send_ids[sd], cnt + 2,
+                                                                     ctx->ipc_vrecv[sd]);
+        LAUNCHED();
+        CK(cudaMemsetAsync(cnt + 2, 0, sizeof(int), ctx->stream));
+        CK(cudaEventRecord(ctx->ipc_free[sd], ctx->stream));
+        break;
+    }
   }
   return 0;
 }

@@ -194,6 +194,49 @@ class TorchExchange:
         return self._sendrecv(mine, {nb: (recv_counts[nb], width) for nb in recv_counts}, dtype)
 
 
+class IpcExchange:
+    """Peer-memory halo exchange between neighbouring ranks: each window maps
+    its neighbours' receive buffers and events (CUDA IPC; NVLink P2P between
+    GPUs) and the pack kernels write straight into them (mpm_ipc_halo), so
+    per substep only two host barriers remain.  Migration at re-binning and
+    the one-time handle exchange go through torch.distributed."""
+
+    def __init__(self, window, rank, world, device="cuda"):
+        self.host = TorchExchange(window, rank, world, device)
+        self.win, self.rank, self.world, self.device = window, rank, world, device
+        self.sides = None
+
+    def connect(self, ctx):
+        """Export our buffers / events, map the neighbours' (collective: every
+        rank calls it once, when its window's context exists)."""
+        import torch.distributed as dist
+        if self.sides is not None:
+            return
+        L = _lib.lib()
+        size = int(L.mpm_ipc_blob_size())
+        blobs = {}
+        for side in (0, 1):
+            buf = ctypes.create_string_buffer(size)
+            ctx.call("mpm_ipc_export", side, buf)
+            blobs[side] = buf.raw
+        every = [None] * self.world
+        dist.all_gather_object(every, blobs)
+        self.sides = 0
+        for side, nb in _neighbours(self.rank, self.world).items():
+            ctx.call("mpm_ipc_import", side, every[nb][1 - side])
+            self.sides |= 1 << side
+        dist.barrier()
+
+    def counts(self, mine):
+        return self.host.counts(mine)
+
+    def _sendrecv(self, send, recv_shapes, dtype):
+        return self.host._sendrecv(send, recv_shapes, dtype)
+
+    def halo(self, ctx, phase):
+        ctx.call("mpm_ipc_halo", phase, self.sides)
+
+
 def step_local(windows, exchange: LocalExchange, materials, params, colliders=None, pose_rows=None):
     """One frame (params.substeps_per_frame substeps) of every window in this process."""
     nsub = params.substeps_per_frame
@@ -317,11 +360,16 @@ def _halo_exchange(win: SlabWindow, ex: TorchExchange, counts: dict, with_ids: b
     return {side: recv.get(side, 0) for side in (0, 1)}
 
 
-def step_distributed(win: SlabWindow, ex: TorchExchange, materials, params, colliders=None, pose_rows=None):
-    """One frame for this rank's window; halos/migrants travel over torch.distributed."""
+def step_distributed(win: SlabWindow, ex, materials, params, colliders=None, pose_rows=None):
+    """One frame for this rank's window; halos travel through the exchange
+    (TorchExchange: torch.distributed point-to-point; IpcExchange: the pack
+    kernels write into the neighbours' mapped buffers), migrants over
+    torch.distributed."""
     import torch
     L = _lib.lib()
     ctx = win.configure(materials, params, colliders, pose_rows)
+    if isinstance(ex, IpcExchange):
+        ex.connect(ctx)
     nsub = params.substeps_per_frame
     span_max = int(params.rebin_interval)
     inverted = 0
@@ -332,6 +380,16 @@ def step_distributed(win: SlabWindow, ex: TorchExchange, materials, params, coll
         for t in range(span):
             sub = s + t
             ctx.call("mpm_stage_particles", int(t == 0))
+            if isinstance(ex, IpcExchange):
+                import torch.distributed as dist
+                ex.halo(ctx, 0)
+                dist.barrier()
+                ex.halo(ctx, 1)
+                ctx.call("mpm_stage_grid", sub, int(sub != nsub - 1))
+                ex.halo(ctx, 2)
+                dist.barrier()
+                ex.halo(ctx, 3)
+                continue
             counts = {}
             for side in (0, 1):
                 n = ctypes.c_int64()

@@ -1,8 +1,10 @@
-"""Config 5 multi-process path: two ranks (gloo, host-staged exchange) each
-own one x-slab window and step it with slab.step_distributed -- the same code
-path as NCCL across GPUs, here as two processes sharing one GPU (the ranks'
-kernels never wait on each other; every exchange goes through the host).
-The gathered state must reproduce the undecomposed run."""
+"""Config 5 multi-process path: two ranks each own one x-slab window and step
+it with slab.step_distributed, as two processes sharing one GPU -- through
+TorchExchange (gloo, host-staged; the NCCL code path across GPUs) and through
+IpcExchange (the pack kernels write into the neighbour's IPC-mapped buffers;
+NVLink P2P across GPUs).  The ranks' kernels never spin on each other: every
+cross-process dependency is an interprocess event wait ordered by a host
+barrier.  The gathered state must reproduce the undecomposed run."""
 import os
 import socket
 import tempfile
@@ -31,7 +33,7 @@ def _scene(n=24000, res=64, seed=3):
         st.material_id.copy()
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, kind):
     import torch.distributed as dist
     from paper_2402_01181_b200 import slab
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -40,8 +42,11 @@ def _worker(rank, world, port, out_dir):
         params = sm.SimParams(rebin_interval=5)
         wins = slab.split_state(grid, x, v, F, C, m, vol, mat, ranks=world, ghost_bricks=2, device=0)
         win = wins[rank]
-        ex = slab.TorchExchange(win, rank, world, device="cuda:0")
-        assert ex.host_staging
+        if kind == "ipc":
+            ex = slab.IpcExchange(win, rank, world, device="cuda:0")
+        else:
+            ex = slab.TorchExchange(win, rank, world, device="cuda:0")
+            assert ex.host_staging
         for _ in range(FRAMES):
             slab.step_distributed(win, ex, mats, params)
         ids, xw, vw, Fw, _ = win.download()
@@ -56,11 +61,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_process_slab_matches_single_domain():
+@pytest.mark.parametrize("kind", ["torch", "ipc"])
+def test_two_process_slab_matches_single_domain(kind):
     import torch.multiprocessing as mp
     world = 2
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), d, kind), nprocs=world, join=True)
         grid, mats, x, v, F, C, m, vol, mat = _scene()
         ref = sm.SimState(grid, x, v, F, C, m, vol, mat)
         params = sm.SimParams(rebin_interval=5)
