@@ -204,3 +204,22 @@ def extract_surface(state: SimState, iso: float, resolution=None) -> SurfaceMesh
     ctx.call("mpm_marching_cubes", _lib.ptr(None), _lib.ptr(None, _lib._I32), ctypes.c_double(dx),
              ctypes.c_double(iso), ctypes.byref(nv), ctypes.byref(nt))
     return compute_uvs(_fetch_mesh(ctx, nv.value, nt.value), state.grid.extent)
+
+
+def export_obj(mesh: SurfaceMesh, path) -> None:
+    """Wavefront OBJ of a surface mesh (surfacing.py:115-116): `v` lines, then
+    `vt` / `vn` when present (parallel to the vertices), 1-based faces with
+    the matching v/vt/vn references."""
+    from pathlib import Path
+    v = np.asarray(mesh.vertices, dtype=np.float64).reshape(-1, 3)
+    f = np.asarray(mesh.indices, dtype=np.int64).reshape(-1, 3) + 1
+    parts = ["\n".join(f"v {a:.9g} {b:.9g} {c:.9g}" for a, b, c in v)]
+    has_t = mesh.uvs is not None and len(mesh.uvs) == len(v)
+    has_n = mesh.normals is not None and len(mesh.normals) == len(v)
+    if has_t:
+        parts.append("\n".join(f"vt {a:.9g} {b:.9g}" for a, b in np.asarray(mesh.uvs).reshape(-1, 2)))
+    if has_n:
+        parts.append("\n".join(f"vn {a:.9g} {b:.9g} {c:.9g}" for a, b, c in np.asarray(mesh.normals).reshape(-1, 3)))
+    tag = "{0}/{0}/{0}" if has_t and has_n else "{0}/{0}" if has_t else "{0}//{0}" if has_n else "{0}"
+    parts.append("\n".join("f " + " ".join(tag.format(i) for i in tri) for tri in f))
+    Path(path).write_text("\n".join(p for p in parts if p) + "\n", encoding="utf-8")
