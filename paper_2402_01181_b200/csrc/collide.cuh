@@ -17,6 +17,12 @@
 namespace mpm {
 
 constexpr int MAX_COLLIDERS = 16;
+#ifdef FUSED_PROFILE
+__device__ unsigned long long g_cph[4];  // contact phases: nearest, pre-normal, normal, rest (cycles)
+#define CPH_MARK(k, t) do { const long long _t = clock64(); atomicAdd(&g_cph[k], (unsigned long long)(_t - (t))); t = _t; } while (0)
+#else
+#define CPH_MARK(k, t) do { } while (0)
+#endif
 
 struct ColliderGeo {
   int kind;  // 0 box, 1 baked
@@ -67,7 +73,30 @@ __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
+// The reference's sqrt(ox*ox + oy*oy + oz*oz) for ox, oy, oz >= +0 without
+// the library square root when at most one term is non-zero: in radix 2,
+// sqrt(RN(x*x)) == |x| absent under/overflow, and adding +0 is exact, so the
+// result is that term bit for bit.  Near a face (the common contact case)
+// this keeps the branchy sqrt sequence -- which serialises everything around
+// it -- out of the six finite-difference evaluations of world_normal.
+// `ok` is false when the full square root is needed.
+__device__ __forceinline__ double box_sd_fast(double px, double py, double pz, const double h[3], bool& ok) {
+  const double qx = ds(fabs(px), h[0]), qy = ds(fabs(py), h[1]), qz = ds(fabs(pz), h[2]);
+  const bool ax = qx > 0.0, ay = qy > 0.0, az = qz > 0.0;
+  // the one positive term (adding the +0 others is exact): selects, no adds
+  const double one = ax ? qx : ay ? qy : az ? qz : 0.0;
+  ok = (int)ax + (int)ay + (int)az <= 1 && (one == 0.0 || (one > 1e-150 && one < 1e150));
+  double qm = qx;
+  if (qy > qm) qm = qy;
+  if (qz > qm) qm = qz;
+  // outside + inside: one of the two is +0 (a positive term makes qm > 0)
+  return one > 0.0 ? one : (qm < 0.0 ? qm : 0.0);
+}
+
 __device__ inline double box_sd(double px, double py, double pz, const double h[3]) {
+  bool ok;
+  const double fast = box_sd_fast(px, py, pz, h, ok);
+  if (ok) return fast;
   double qx = ds(fabs(px), h[0]), qy = ds(fabs(py), h[1]), qz = ds(fabs(pz), h[2]);
   double ox = qx > 0.0 ? qx : 0.0, oy = qy > 0.0 ? qy : 0.0, oz = qz > 0.0 ? qz : 0.0;
   double outside = __dsqrt_rn(da(da(dm(ox, ox), dm(oy, oy)), dm(oz, oz)));
@@ -236,9 +265,38 @@ __device__ inline void world_normal(const Colliders& cs, int ci, double wx, doub
   } else {
     h = __ddiv_rn(g.sdf_ext, (double)g.sdf_res[0]);
   }
-  double gx = ds(local_sd(g, cs.sdf, da(px, h), py, pz), local_sd(g, cs.sdf, ds(px, h), py, pz));
-  double gy = ds(local_sd(g, cs.sdf, px, da(py, h), pz), local_sd(g, cs.sdf, px, ds(py, h), pz));
-  double gz = ds(local_sd(g, cs.sdf, px, py, da(pz, h)), local_sd(g, cs.sdf, px, py, ds(pz, h)));
+  double gx, gy, gz;
+  if (g.kind == 0) {
+    // six straight-line evaluations; the exact square roots only at edges
+    bool ok[6];
+    const double s0 = box_sd_fast(da(px, h), py, pz, g.half, ok[0]), s1 = box_sd_fast(ds(px, h), py, pz, g.half, ok[1]);
+    const double s2 = box_sd_fast(px, da(py, h), pz, g.half, ok[2]), s3 = box_sd_fast(px, ds(py, h), pz, g.half, ok[3]);
+    const double s4 = box_sd_fast(px, py, da(pz, h), g.half, ok[4]), s5 = box_sd_fast(px, py, ds(pz, h), g.half, ok[5]);
+    gx = ds(s0, s1);
+    gy = ds(s2, s3);
+    gz = ds(s4, s5);
+    if (!(ok[0] && ok[1] && ok[2] && ok[3] && ok[4] && ok[5])) {
+      gx = ds(box_sd(da(px, h), py, pz, g.half), box_sd(ds(px, h), py, pz, g.half));
+      gy = ds(box_sd(px, da(py, h), pz, g.half), box_sd(px, ds(py, h), pz, g.half));
+      gz = ds(box_sd(px, py, da(pz, h), g.half), box_sd(px, py, ds(pz, h), g.half));
+    }
+  } else {
+    gx = ds(baked_sd(g, cs.sdf, da(px, h), py, pz), baked_sd(g, cs.sdf, ds(px, h), py, pz));
+    gy = ds(baked_sd(g, cs.sdf, px, da(py, h), pz), baked_sd(g, cs.sdf, px, ds(py, h), pz));
+    gz = ds(baked_sd(g, cs.sdf, px, py, da(pz, h)), baked_sd(g, cs.sdf, px, py, ds(pz, h)));
+  }
+  // axis-aligned gradient (a face): norm = |g| exactly (see box_sd_fast) and
+  // g / norm = (+-1, +-0, +-0) -- the divisions are exact, so skip them
+  const double ag = gx != 0.0 ? fabs(gx) : gy != 0.0 ? fabs(gy) : fabs(gz);
+  if ((int)(gx != 0.0) + (int)(gy != 0.0) + (int)(gz != 0.0) == 1 && ag >= 1.0e-12 && ag < 1e150) {
+    gx = gx > 0.0 ? 1.0 : gx < 0.0 ? -1.0 : gx;
+    gy = gy > 0.0 ? 1.0 : gy < 0.0 ? -1.0 : gy;
+    gz = gz > 0.0 ? 1.0 : gz < 0.0 ? -1.0 : gz;
+    n[0] = da(da(dm(q.R[0], gx), dm(q.R[1], gy)), dm(q.R[2], gz));
+    n[1] = da(da(dm(q.R[3], gx), dm(q.R[4], gy)), dm(q.R[5], gz));
+    n[2] = da(da(dm(q.R[6], gx), dm(q.R[7], gy)), dm(q.R[8], gz));
+    return;
+  }
   double norm = __dsqrt_rn(da(da(dm(gx, gx), dm(gy, gy)), dm(gz, gz)));
   if (norm < 1.0e-12) {
     double fx = ds(wx, q.T[0]), fy = ds(wy, q.T[1]), fz = ds(wz, q.T[2]);
@@ -259,6 +317,9 @@ __device__ inline void world_normal(const Colliders& cs, int ci, double wx, doub
 // Contact response at a massive node inside the band (kernels.py:371-411).
 __device__ inline void resolve_contact(const Colliders& cs, int ci, double wx, double wy, double wz,
                                        double v[3]) {
+#ifdef FUSED_PROFILE
+  long long tp = clock64();
+#endif
   const ColliderPose& q = cs.pose[ci];
   double rx = ds(wx, q.T[0]), ry = ds(wy, q.T[1]), rz = ds(wz, q.T[2]);
   double co0 = ds(da(q.lv[0], dm(q.av[1], rz)), dm(q.av[2], ry));
@@ -266,7 +327,9 @@ __device__ inline void resolve_contact(const Colliders& cs, int ci, double wx, d
   double co2 = ds(da(q.lv[2], dm(q.av[0], ry)), dm(q.av[1], rx));
   double r0 = ds(v[0], co0), r1 = ds(v[1], co1), r2 = ds(v[2], co2);
   double n[3];
+  CPH_MARK(1, tp);
   world_normal(cs, ci, wx, wy, wz, n);
+  CPH_MARK(2, tp);
   double vn = da(da(dm(r0, n[0]), dm(r1, n[1])), dm(r2, n[2]));
   if (!(vn < 0.0)) return;
   if (q.mode == 1) {

@@ -25,7 +25,8 @@ namespace mpm {
 #ifdef FUSED_PROFILE
 __device__ unsigned long long g_fprof[6];
 __device__ unsigned long long g_fcnt[4];  // particles, G2P off-tile, P2G fallback
-__device__ unsigned long long g_gprof[8];  // grid op: sum / max CTA ns, CTAs, launches, sum of per-launch max, clearing launches, bricks
+__device__ unsigned long long g_gprof[8];
+__device__ unsigned long long g_cprof[4];  // grid contact: warp calls, lanes, cycles, max cycles  // grid op: sum / max CTA ns, CTAs, launches, sum of per-launch max, clearing launches, bricks
 #define FPROF_COUNT(k) atomicAdd(&g_fcnt[k], 1ull)
 #else
 #define FPROF_COUNT(k)
@@ -990,10 +991,15 @@ __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
 __device__ __noinline__ float3 grid_contact(const Colliders cs, double cap, double wx, double wy, double wz, float v0,
                                             float v1, float v2) {
   double best;
+#ifdef FUSED_PROFILE
+  long long tq = clock64();
+#endif
   const int ci = nearest_collider(cs, wx, wy, wz, cap, best);
+  CPH_MARK(0, tq);
   if (best < cs.theta && ci >= 0) {
     double vv[3] = {v0, v1, v2};
     resolve_contact(cs, ci, wx, wy, wz, vv);
+    CPH_MARK(3, tq);
     return make_float3((float)vv[0], (float)vv[1], (float)vv[2]);
   }
   return make_float3(v0, v1, v2);
@@ -1036,7 +1042,20 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
       for (int ci = 0; ci < cs.count; ++ci) near |= collider_near(cs, ci, fx, fy, fz, cs.theta_f);
     }
     if (near) {
+#ifdef FUSED_PROFILE
+      const long long c0 = clock64();
+#endif
       const float3 v = grid_contact(cs, cap, (double)gi * p.dx64, (double)gj * p.dx64, (double)gk * p.dx64, v0, v1, v2);
+#ifdef FUSED_PROFILE
+      const long long c1 = clock64();
+      const unsigned m = __activemask();
+      if ((int)(threadIdx.x & 31) == __ffs(m) - 1) {
+        atomicAdd(&g_cprof[0], 1ull);
+        atomicAdd(&g_cprof[1], (unsigned long long)__popc(m));
+        atomicAdd(&g_cprof[2], (unsigned long long)(c1 - c0));
+        atomicMax(&g_cprof[3], (unsigned long long)(c1 - c0));
+      }
+#endif
       v0 = v.x;
       v1 = v.y;
       v2 = v.z;

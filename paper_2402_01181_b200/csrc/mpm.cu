@@ -799,6 +799,15 @@ int mpm_destroy(mpm_ctx* ctx) {
       fprintf(stderr, "[grid profile] launches %llu  mean CTA %.2f us  mean per-launch max CTA %.2f us (clearing launches %llu, bricks/launch %.0f)  CTAs/launch %llu\n",
               g[3], g[0] / (double)(g[2] ? g[2] : 1) / 1e3, g[4] / (double)(g[5] ? g[5] : 1) / 1e3, g[5],
               g[6] / (double)(g[5] ? g[5] : 1), g[2] / g[3]);
+    unsigned long long cc[4];
+    cudaMemcpyFromSymbol(cc, g_cprof, sizeof(cc));
+    if (g[3])
+      fprintf(stderr, "[contact profile] warp calls/launch %.1f  lanes/call %.1f  cycles/call %.0f  max %llu\n",
+              cc[0] / (double)g[3], cc[1] / (double)(cc[0] ? cc[0] : 1), cc[2] / (double)(cc[0] ? cc[0] : 1), cc[3]);
+    unsigned long long ph[4];
+    cudaMemcpyFromSymbol(ph, g_cph, sizeof(ph));
+    fprintf(stderr, "[contact phases] thread-cycles: nearest %.3e  pre-normal %.3e  normal %.3e  nearest->end %.3e\n",
+            (double)ph[0], (double)ph[1], (double)ph[2], (double)ph[3]);
     unsigned long long c[4];
     cudaMemcpyFromSymbol(c, g_fcnt, sizeof(c));
     fprintf(stderr, "[fused profile] particles %llu  g2p off-tile %llu (%.4f)  p2g fallback %llu (%.4f, bound %llu)\n",
