@@ -216,6 +216,13 @@ int mpm_splat_density_host(int device, const double *positions, const double *ma
 int mpm_marching_cubes(mpm_ctx *ctx, const double *values, const int32_t *res, double dx, double iso,
                        int64_t *nverts, int64_t *ntris);
 int mpm_mesh_fetch(mpm_ctx *ctx, double *verts, int32_t *tris, double *normals);
+/* encode_frame (server.py:65-92) body from the last mesh, packed on the device:
+ * f32 vertices (3V), f32 normals (3V), f32 planar UVs (2V; compute_uvs,
+ * surfacing.py:92-101, against extent[3]) and u32 triangle indices (3T),
+ * little-endian, back to back -- 32 V + 12 T bytes into out (host memory,
+ * cap bytes).  *len receives the size; out = NULL only queries it.  The MPMF
+ * header and collider records around it are assembled by the caller. */
+int mpm_mesh_encode(mpm_ctx *ctx, const double *extent, uint8_t *out, int64_t cap, int64_t *len);
 /* Per-kernel CUDA-event timing on the context stream (bench/roofline).
  * When enabled every fast-path launch is bracketed by events; mpm_get_timing
  * fills out[16] = {g2p_stress_ms, g2p_stress_launches, grid_op_ms,

@@ -39,7 +39,7 @@ EXPORTS = (
     "mpm_halo_unpack_add", "mpm_halo_pack_vel", "mpm_halo_unpack_vel", "mpm_extract_migrants",
     "mpm_append_particles", "mpm_reserve", "mpm_download_ids", "mpm_device_copy", "mpm_set_ids",
     "mpm_download_rows", "mpm_metrics", "mpm_splat_density", "mpm_splat_density_host",
-    "mpm_marching_cubes", "mpm_mesh_fetch", "mpm_ipc_blob_size", "mpm_ipc_export", "mpm_ipc_import",
+    "mpm_marching_cubes", "mpm_mesh_fetch", "mpm_mesh_encode", "mpm_ipc_blob_size", "mpm_ipc_export", "mpm_ipc_import",
     "mpm_ipc_halo",
 )
 
@@ -126,6 +126,7 @@ def lib():
     L.mpm_splat_density_host.argtypes = [ctypes.c_int, _D, _D, ctypes.c_int64, _I32, ctypes.c_double, _D]
     L.mpm_marching_cubes.argtypes = [_VP, _D, _I32, ctypes.c_double, ctypes.c_double, _I64, _I64]
     L.mpm_mesh_fetch.argtypes = [_VP, _D, _I32, _D]
+    L.mpm_mesh_encode.argtypes = [_VP, _D, _VP, ctypes.c_int64, _I64]
     L.mpm_ipc_blob_size.restype = ctypes.c_int64
     L.mpm_ipc_export.argtypes = [_VP, ctypes.c_int, ctypes.c_char_p]
     L.mpm_ipc_import.argtypes = [_VP, ctypes.c_int, ctypes.c_char_p]

@@ -1891,6 +1891,30 @@ __global__ void mc_cell_emit_kernel(const double* __restrict__ f, int nx, int ny
   }
 }
 
+// MPMF frame body (server.py:65-92) from the device mesh: f32 vertices, f32
+// normals, f32 planar UVs (surfacing.py:92-101: u = clip(x / ext0, 0, 1),
+// v = clip(z / ext2, 0, 1), in fp64 then rounded like numpy's astype) and u32
+// triangle indices, each array contiguous and little-endian, back to back.
+__global__ void mesh_encode_kernel(const double* __restrict__ v, const double* __restrict__ nrm, long long nv,
+                                   const int* __restrict__ tris, long long nt, double ext0, double ext2,
+                                   float* __restrict__ ov, float* __restrict__ on, float* __restrict__ ouv,
+                                   unsigned* __restrict__ ot) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * nv; i += stride) {
+    ov[i] = __double2float_rn(v[i]);
+    on[i] = __double2float_rn(nrm[i]);
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    double u = __ddiv_rn(v[3 * i], ext0), w = __ddiv_rn(v[3 * i + 2], ext2);
+    u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
+    w = w < 0.0 ? 0.0 : (w > 1.0 ? 1.0 : w);
+    ouv[2 * i] = __double2float_rn(u);
+    ouv[2 * i + 1] = __double2float_rn(w);
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * nt; i += stride)
+    ot[i] = (unsigned)tris[i];
+}
+
 // ---------------------------------------------------------------------------
 // slab decomposition (config 5): sparse ghost-brick exchange + migration
 // ---------------------------------------------------------------------------

@@ -105,6 +105,8 @@ struct mpm_ctx {
   int* mc_off = nullptr;
   long long mc_cap = 0;
   double* mesh_v = nullptr;  // vertices, then normals
+  unsigned char* enc = nullptr;  // encoded frame body
+  long long enc_cap = 0;
   int* mesh_t = nullptr;
   long long mesh_nv = 0, mesh_nt = 0, mesh_vcap = 0, mesh_tcap = 0;
   long long x0_n = -1;
@@ -828,7 +830,7 @@ int mpm_destroy(mpm_ctx* ctx) {
                   ctx->h_recv_data[1], ctx->h_local_ids[0], ctx->h_local_ids[1],
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
                   ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
-                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag, ctx->x0, ctx->field, ctx->mc_flag, ctx->mc_vid, ctx->mc_cnt, ctx->mc_off, ctx->mesh_v, ctx->mesh_t};
+                  ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag, ctx->x0, ctx->field, ctx->mc_flag, ctx->mc_vid, ctx->mc_cnt, ctx->mc_off, ctx->mesh_v, ctx->mesh_t, ctx->enc};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int* b : ctx->scan_tmp)
@@ -1506,6 +1508,32 @@ int mpm_mesh_fetch(mpm_ctx* ctx, double* verts, int32_t* tris, double* normals) 
   if (normals && nv)
     CK(cudaMemcpyAsync(normals, ctx->mesh_v + 3 * nv, sizeof(double) * 3 * nv, cudaMemcpyDeviceToHost, ctx->stream));
   if (tris && nt) CK(cudaMemcpyAsync(tris, ctx->mesh_t, sizeof(int) * 3 * nt, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int mpm_mesh_encode(mpm_ctx* ctx, const double* extent, uint8_t* out, int64_t cap, int64_t* len) {
+  if (!ctx || !extent || !len) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  const long long nv = ctx->mesh_nv, nt = ctx->mesh_nt;
+  const long long bytes = 32 * nv + 12 * nt;
+  *len = bytes;
+  if (!out) return 0;  // size query
+  if (cap < bytes) return fail(ctx, MPM_EINVAL, "mesh_encode: output buffer too small");
+  if (!bytes) return 0;
+  if (ctx->enc_cap < bytes) {
+    TRY(dalloc(ctx, &ctx->enc, (size_t)bytes));
+    ctx->enc_cap = bytes;
+  }
+  float* ov = reinterpret_cast<float*>(ctx->enc);
+  float* on = ov + 3 * nv;
+  float* ouv = on + 3 * nv;
+  unsigned* ot = reinterpret_cast<unsigned*>(ouv + 2 * nv);
+  const long long work = std::max(3 * nv, 3 * nt);
+  mesh_encode_kernel<<<blocks_for(work, 256), 256, 0, ctx->stream>>>(ctx->mesh_v, ctx->mesh_v + 3 * nv, nv, ctx->mesh_t,
+                                                                     nt, extent[0], extent[2], ov, on, ouv, ot);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, ctx->enc, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }

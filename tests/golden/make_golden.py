@@ -204,7 +204,27 @@ def frame_ops():
                                       m.max_displacement]))
 
 
+def mpmf_frame():
+    """server.encode_frame bytes for a small mesh (with and without normals /
+    UVs) and two collider records, plus the inputs."""
+    from softmpm import server
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1.0, 2.0, (37, 3))
+    n = rng.normal(size=(37, 3))
+    uv = rng.uniform(0.0, 1.0, (37, 2))
+    t = rng.integers(0, 37, (50, 3)).astype(np.int32)
+    cols = [server.ColliderPose(0, np.array([0.1, 0.2, 0.3]), np.array([0.0, 0.0, 0.0, 1.0]), False),
+            server.ColliderPose(5, np.array([-1.5, 2.25, 1e-3]), np.array([0.1, -0.2, 0.3, 0.927]), True)]
+    full = server.encode_frame(sm.SurfaceMesh(vertices=v, indices=t, uvs=uv, normals=n), cols, 42, 1.0 / 3.0)
+    bare = server.encode_frame(sm.SurfaceMesh(vertices=v, indices=t), [], 7, 0.5)
+    np.savez_compressed(os.path.join(OUT, "mpmf_frame.npz"), v=v, n=n, uv=uv, t=t,
+                        col_id=np.array([c.id for c in cols]), col_t=np.array([c.translation for c in cols]),
+                        col_q=np.array([c.quaternion for c in cols]), col_jaw=np.array([c.jaw_closed for c in cols]),
+                        full=np.frombuffer(full, np.uint8), bare=np.frombuffer(bare, np.uint8))
+
+
 if __name__ == "__main__":
+    mpmf_frame()
     frame_ops()
     substep_colliders()
     floor_block()

@@ -122,3 +122,24 @@ def test_extract_surface_of_a_device_state():
     edges = _directed_edges(mesh.indices)
     for a, b in edges:
         assert (b, a) in edges
+
+
+def test_encode_surface_frame_equals_host_encoding():
+    """the frame body packed on the device from the device
+    mesh equals encode_frame(extract_surface(...)) byte for byte."""
+    grid = sm.Grid(resolution=(24, 24, 24), extent=(1.0, 1.0, 1.0))
+    mats = [sm.Material(1.0e4, 0.3, 1000.0)]
+    spawn = sm.sample_box((0.45, 0.4, 0.55), (0.3, 0.25, 0.3), 12000, seed=5, grid=grid)
+    st = sm.SimState.from_spawns(grid, [spawn], mats)
+    sm.step(st, mats, sm.SimParams())
+    cols = [sm.wire.ColliderPose(2, np.array([0.5, 0.7, 0.5]), np.array([0.0, 0.0, 0.0, 1.0]), True)]
+    dev = sm.encode_surface_frame(st, 300.0, cols, 9, float(st.time))
+    host = sm.encode_frame(sm.extract_surface(st, 300.0), cols, 9, float(st.time))
+    assert len(dev) > 1000 and dev == host
+    d = sm.decode_frame(dev)
+    assert len(d.vertices) > 0 and d.colliders[0].id == 2
+    # resolution override and a surface that never reaches the iso level
+    assert sm.encode_surface_frame(st, 300.0, [], 1, 0.0, resolution=(32, 32, 32)) == \
+        sm.encode_frame(sm.extract_surface(st, 300.0, resolution=(32, 32, 32)), [], 1, 0.0)
+    empty = sm.encode_surface_frame(st, 1e12, [], 3, 0.0)
+    assert sm.decode_frame(empty).vertices.shape == (0, 3)
