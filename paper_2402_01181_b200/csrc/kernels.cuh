@@ -22,11 +22,23 @@ namespace cg = cooperative_groups;
 
 namespace mpm {
 
+// Programmatic dependent launch (the fused kernel and the grid op alternate
+// within a substep stretch): a kernel launched with programmatic stream
+// serialization may start while its predecessor drains; griddep_wait() blocks
+// until the predecessor has completed and its writes are visible, and
+// griddep_trigger() lets the successor's CTAs be scheduled.  Each kernel
+// triggers only after its own wait, so at most two kernels overlap and the
+// code before a wait may read anything produced two launches back.  Both are
+// no-ops in a normal launch.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 #ifdef FUSED_PROFILE
 __device__ unsigned long long g_fprof[6];
 __device__ unsigned long long g_fcnt[4];  // particles, G2P off-tile, P2G fallback
-__device__ unsigned long long g_gprof[8];
-__device__ unsigned long long g_cprof[4];  // grid contact: warp calls, lanes, cycles, max cycles  // grid op: sum / max CTA ns, CTAs, launches, sum of per-launch max, clearing launches, bricks
+__device__ unsigned long long g_gprof[8];  // grid op: sum / max CTA ns, CTAs, launches, sum of per-launch max, clearing launches, bricks
+__device__ unsigned long long g_cprof[4];  // grid contact: warp calls, lanes, cycles, max cycles
+__device__ unsigned long long g_gwin[4] = {~0ull, 0ull, 0ull, 0ull};  // grid op window: min start, max end, sum of windows, max start
 #define FPROF_COUNT(k) atomicAdd(&g_fcnt[k], 1ull)
 #else
 #define FPROF_COUNT(k)
@@ -793,7 +805,7 @@ __device__ __forceinline__ long long fprof_clock_dep(int dep) {
 // the int32 tile is cleared first (the flushes leave it clean afterwards).
 __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict__ bounds_in,
                                             float4* __restrict__ bounds_out, int* __restrict__ item_box,
-                                            bool zero_tile) {
+                                            bool zero_tile, bool dep_wait = false) {
   extern __shared__ float smem[];
   float* vtile = smem;                                           // 3 x TILE_NODES
   int* tile = reinterpret_cast<int*>(smem + 3 * TILE_NODES);     // 4 x TILE_NODES
@@ -811,14 +823,20 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
   int par = 0;
   // dynamic scheduling over the size-sorted work list: the first gridDim.x
   // items are taken in launch order, later ones from the counter
+  // (work list, item boxes and bounds come from launches before the grid op:
+  // read before the dependency wait; grid velocities, gm, counters after it)
   if (blockIdx.x < nwork) {
     TileVel tv0;
     const int4 it0 = p.work[blockIdx.x];
     fused_item_geometry(p, it0, item_box[blockIdx.x], tv0);
-    fused_item_vtile_issue(p, tv0, vtile);
     fused_item_scales(it0, bounds_in[blockIdx.x], scale_s[0]);
+    if (dep_wait) griddep_wait();
+    fused_item_vtile_issue(p, tv0, vtile);
     cp_async_wait_all();
+  } else if (dep_wait) {
+    griddep_wait();
   }
+  if (dep_wait) griddep_trigger();
   __syncthreads();  // [A] first velocity tile + scales ready
 #ifdef FUSED_PROFILE
   unsigned long long pr[5] = {0, 0, 0, 0, 0};
@@ -964,7 +982,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
 __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,
                                                                                   float4* __restrict__ bounds_out,
                                                                                   int* __restrict__ item_box) {
-  fused_phase(p, bounds_in, bounds_out, item_box, true);
+  fused_phase(p, bounds_in, bounds_out, item_box, true, true);
 }
 
 // Final G2P of a frame / stage g2p_advect: thread per particle.
@@ -1079,19 +1097,31 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
 // The grid op as a CTA-level phase (grid_op_kernel, and once per substep in
 // the cooperative substeps_kernel).
 template <bool DENSE>
-__device__ __forceinline__ void grid_phase(const Params& p, const Colliders& cs, int clear) {
+__device__ __forceinline__ void grid_phase(const Params& p, const Colliders& cs, int clear, bool dep_wait = false) {
   // one table for the whole grid: the fp32 prefilter boxes are staged in
   // shared memory once per CTA (per-environment tables use collider_near)
   __shared__ ColliderNearF nf_s[MAX_COLLIDERS];
   const bool staged = !cs.per_env && cs.theta >= 0.0 && cs.count > 0 && cs.count <= MAX_COLLIDERS;
   if (staged && threadIdx.x < cs.count) nf_s[threadIdx.x] = make_near_f(cs, threadIdx.x, cs.theta_f);
+  // collider tables come from the host: staged before the dependency wait
+  if (dep_wait) {
+    griddep_wait();
+    griddep_trigger();
+  }
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long first = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const long long nbt = (long long)p.nb[0] * p.nb[1] * p.nb[2];
+  // the brick count and this warp's first 32 list entries are loaded
+  // together (entries past the count are ignored): one dependent round trip
+  // to the first momentum loads instead of two
+  const long long spec_it = first + (long long)lane * stride;
+  const int spec_b = !DENSE && spec_it < nbt ? p.active_list[spec_it] : 0;
+  const long long nitems = DENSE ? nbt : (long long)*p.active_count;
   __syncthreads();
   const ColliderNearF* nf = staged ? nf_s : nullptr;
   const bool single_env = p.env_res[0] == p.gres[0] && p.env_res[1] == p.gres[1] && p.env_res[2] == p.gres[2];
-  const long long nitems = DENSE ? (long long)p.nb[0] * p.nb[1] * p.nb[2] : (long long)*p.active_count;
-  const int lane = threadIdx.x & 31;
   const double cap = 2.0 * cs.theta;
-  const long long stride = (long long)gridDim.x * (blockDim.x >> 5);
   const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
   // this warp's bricks: first, first + stride, ... (strided so that the
   // expensive contact bricks, clustered in the list, spread over warps).
@@ -1100,12 +1130,11 @@ __device__ __forceinline__ void grid_phase(const Params& p, const Colliders& cs,
   // warp-major numbering (warp w of CTA c is w * gridDim + c): consecutive
   // list entries -- one item's bricks, e.g. a tool's contact band -- land in
   // different CTAs / SMs instead of the 8 warps of one CTA
-  const long long first = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const long long nmine = nitems > first ? (nitems - first + stride - 1) / stride : 0;
   for (long long base = 0; base < nmine; base += 32) {
     const int cnt = (int)min(32LL, nmine - base);
     const long long my_it = first + (base + lane) * stride;
-    const int myb = lane < cnt ? (DENSE ? (int)my_it : p.active_list[my_it]) : 0;
+    const int myb = lane < cnt ? (DENSE ? (int)my_it : (base == 0 ? spec_b : p.active_list[my_it])) : 0;
     long long b0 = __shfl_sync(0xffffffffu, myb, 0), b1 = __shfl_sync(0xffffffffu, myb, cnt > 1 ? 1 : 0);
     float4 a00 = p.gm[(b0 << 6) | lane], a01 = p.gm[((b0 << 6) | lane) + 32];
     float4 a10 = a00, a11 = a01;
@@ -1150,13 +1179,16 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   unsigned long long g_t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
 #endif
-  grid_phase<DENSE>(p, cs, clear);
+  grid_phase<DENSE>(p, cs, clear, true);
 #ifdef FUSED_PROFILE
   {
     __syncthreads();
     unsigned long long g_t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t1));
     if (threadIdx.x == 0) {
+      atomicMin(&g_gwin[0], g_t0);
+      atomicMax(&g_gwin[1], g_t1);
+      atomicMax(&g_gwin[3], g_t0);
       atomicAdd(&g_gprof[0], g_t1 - g_t0);
       atomicMax(&g_gprof[1], g_t1 - g_t0);
       atomicAdd(&g_gprof[2], 1ull);
@@ -1168,18 +1200,23 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   // and work-item counters for the next substep (no memset nodes per substep)
   if (done) {
     __syncthreads();
+    // (every CTA read the counters before its increment; the next launch
+    // sees the reset across the kernel boundary: no fences needed)
     if (threadIdx.x == 0) {
-      __threadfence();
       if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
 #ifdef FUSED_PROFILE
         atomicAdd(&g_gprof[4], atomicExch(&g_gprof[1], 0ull));
         atomicAdd(&g_gprof[5], 1ull);
         atomicAdd(&g_gprof[6], (unsigned long long)*p.active_count);
+        {
+          const unsigned long long a = atomicExch(&g_gwin[0], ~0ull), b = atomicExch(&g_gwin[1], 0ull);
+          const unsigned long long c = atomicExch(&g_gwin[3], 0ull);
+          atomicAdd(&g_gwin[2], ((b - a) << 20) | min(c - a, (1ull << 20) - 1));  // window ns (hi), start spread ns (lo)
+        }
 #endif
         *p.active_count = 0;
         *p.work_next = 0;
         *done = 0;
-        __threadfence();
       }
     }
   }

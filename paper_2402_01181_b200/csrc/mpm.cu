@@ -168,6 +168,7 @@ struct mpm_ctx {
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
   int items_per_sm = 4;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
   bool mega_on = false;   // substeps 2..L as one cooperative substeps_kernel (option "mega" / SOFTMPM_MEGA=1)
+  bool pdl_on = true;     // fused kernel / grid op with programmatic dependent launch (option "pdl" / SOFTMPM_PDL=0)
   int mega_blocks = 0;
   bool mega_coop = false;  // device supports cooperative launches
   bool counters_clean = true;     // counters[0] (active bricks) and [3] (work_next) known zero
@@ -505,6 +506,25 @@ int rebin(mpm_ctx* ctx) {
   return 0;
 }
 
+// Launch with programmatic stream serialization when enabled: the kernel may
+// be scheduled while its predecessor drains (griddep_wait / griddep_trigger in
+// kernels.cuh order the dependent part).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(mpm_ctx* ctx, void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl_on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // One substep's particle work.  g2p=false: first substep after a re-binning
 // (v, C from memory): stage A<false> (exact bounds + payload) then stage B.
 // g2p=true: the fused steady-state kernel (bounds of the previous substep).
@@ -545,8 +565,8 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   ctx->bounds_out_clean = true;
   {
     TimedRegion tr(ctx, 5);
-    fused_kernel<<<ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, ctx->stream>>>(
-          p, ctx->item_bounds, ctx->item_bounds2, ctx->item_box);
+    CK(launch_pdl(ctx, fused_kernel, ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, p,
+                  ctx->item_bounds, ctx->item_bounds2, ctx->item_box));
     LAUNCHED();
   }
   std::swap(ctx->item_bounds, ctx->item_bounds2);
@@ -559,9 +579,9 @@ int launch_grid_op(mpm_ctx* ctx, bool dense, bool use_col, int row, bool clear) 
   TimedRegion tr(ctx, 1);
   int* done = clear && !dense ? ctx->counters + 63 : nullptr;  // counters reset by the last CTA
   if (dense)
-    grid_op_kernel<true><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0, done);
+    CK(launch_pdl(ctx, grid_op_kernel<true>, ctx->gridop_blocks, 256, 0, p, cs, clear ? 1 : 0, done));
   else
-    grid_op_kernel<false><<<ctx->gridop_blocks, 256, 0, ctx->stream>>>(p, cs, clear ? 1 : 0, done);
+    CK(launch_pdl(ctx, grid_op_kernel<false>, ctx->gridop_blocks, 256, 0, p, cs, clear ? 1 : 0, done));
   LAUNCHED();
   if (done) ctx->counters_clean = true;
   return 0;
@@ -773,6 +793,8 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
       const char* mg = getenv("SOFTMPM_MEGA");
       ctx->mega_coop = coop != 0;
       ctx->mega_on = coop && mg && mg[0] == '1';
+      const char* pd = getenv("SOFTMPM_PDL");
+      if (pd && pd[0] == '0') ctx->pdl_on = false;
     }
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   }
@@ -801,6 +823,11 @@ int mpm_destroy(mpm_ctx* ctx) {
       fprintf(stderr, "[grid profile] launches %llu  mean CTA %.2f us  mean per-launch max CTA %.2f us (clearing launches %llu, bricks/launch %.0f)  CTAs/launch %llu\n",
               g[3], g[0] / (double)(g[2] ? g[2] : 1) / 1e3, g[4] / (double)(g[5] ? g[5] : 1) / 1e3, g[5],
               g[6] / (double)(g[5] ? g[5] : 1), g[2] / g[3]);
+    unsigned long long gw[4];
+    cudaMemcpyFromSymbol(gw, g_gwin, sizeof(gw));
+    if (g[5])
+      fprintf(stderr, "[grid window] first CTA start -> last CTA end %.2f us, start spread %.2f us (per clearing launch)\n",
+              (gw[2] >> 20) / (double)g[5] / 1e3, (gw[2] & ((1ull << 20) - 1)) / (double)g[5] / 1e3);
     unsigned long long cc[4];
     cudaMemcpyFromSymbol(cc, g_cprof, sizeof(cc));
     if (g[3])
@@ -1290,6 +1317,9 @@ int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
     if (value && !ctx->mega_coop) return fail(ctx, MPM_EINVAL, "mega: device has no cooperative launch");
     invalidate_graphs(ctx);
     ctx->mega_on = value != 0;
+  } else if (!strcmp(key, "pdl")) {
+    invalidate_graphs(ctx);
+    ctx->pdl_on = value != 0;
   } else {
     return fail(ctx, MPM_EINVAL, std::string("unknown option ") + key);
   }
