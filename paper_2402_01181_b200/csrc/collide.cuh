@@ -85,7 +85,7 @@ __device__ __forceinline__ double box_sd_fast(double px, double py, double pz, c
   const bool ax = qx > 0.0, ay = qy > 0.0, az = qz > 0.0;
   // the one positive term (adding the +0 others is exact): selects, no adds
   const double one = ax ? qx : ay ? qy : az ? qz : 0.0;
-  ok = (int)ax + (int)ay + (int)az <= 1 && (one == 0.0 || (one > 1e-150 && one < 1e150));
+  ok = ((int)ax + (int)ay + (int)az <= 1) & ((one == 0.0) | ((one > 1e-150) & (one < 1e150)));  // no branches
   double qm = qx;
   if (qy > qm) qm = qy;
   if (qz > qm) qm = qz;
@@ -275,7 +275,7 @@ __device__ inline void world_normal(const Colliders& cs, int ci, double wx, doub
     gx = ds(s0, s1);
     gy = ds(s2, s3);
     gz = ds(s4, s5);
-    if (!(ok[0] && ok[1] && ok[2] && ok[3] && ok[4] && ok[5])) {
+    if (!(ok[0] & ok[1] & ok[2] & ok[3] & ok[4] & ok[5])) {
       gx = ds(box_sd(da(px, h), py, pz, g.half), box_sd(ds(px, h), py, pz, g.half));
       gy = ds(box_sd(px, da(py, h), pz, g.half), box_sd(px, ds(py, h), pz, g.half));
       gz = ds(box_sd(px, py, da(pz, h), g.half), box_sd(px, py, ds(pz, h), g.half));
@@ -288,7 +288,7 @@ __device__ inline void world_normal(const Colliders& cs, int ci, double wx, doub
   // axis-aligned gradient (a face): norm = |g| exactly (see box_sd_fast) and
   // g / norm = (+-1, +-0, +-0) -- the divisions are exact, so skip them
   const double ag = gx != 0.0 ? fabs(gx) : gy != 0.0 ? fabs(gy) : fabs(gz);
-  if ((int)(gx != 0.0) + (int)(gy != 0.0) + (int)(gz != 0.0) == 1 && ag >= 1.0e-12 && ag < 1e150) {
+  if (((int)(gx != 0.0) + (int)(gy != 0.0) + (int)(gz != 0.0) == 1) & (ag >= 1.0e-12) & (ag < 1e150)) {
     gx = gx > 0.0 ? 1.0 : gx < 0.0 ? -1.0 : gx;
     gy = gy > 0.0 ? 1.0 : gy < 0.0 ? -1.0 : gy;
     gz = gz > 0.0 ? 1.0 : gz < 0.0 ? -1.0 : gz;
