@@ -1320,15 +1320,30 @@ __global__ void bin_fill_kernel(const int* key, const int* lcell, const int* ran
 constexpr int LOCAL_CELLS = BIN * BIN * BIN;
 
 // One CTA per bin (grid-stride): counting sort of the bin's slots by local cell.
+// The CTA's bins are screened 256 at a time (one count load per thread) and
+// only the occupied ones visited -- most bins of a sparse scene are empty,
+// and walking them one dependent load at a time dominated the kernel.
 __global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_count, const int* bin_start,
                                                              int nbins, const int* sidx, const int* slc,
                                                              int* rk, int* perm, int* bin_maxcnt) {
   __shared__ int cnt[LOCAL_CELLS];
   __shared__ int wsum[8];
   __shared__ int wmax[8];
-  for (int b = blockIdx.x; b < nbins; b += gridDim.x) {
+  __shared__ int occ[256];
+  __shared__ int nocc;
+  for (long long j0 = 0; (long long)blockIdx.x + j0 * gridDim.x < nbins; j0 += 256) {
+    if (threadIdx.x == 0) nocc = 0;
+    __syncthreads();
+    {
+      const long long b = (long long)blockIdx.x + (j0 + threadIdx.x) * gridDim.x;
+      if (b < nbins && bin_count[b] > 0) occ[atomicAdd(&nocc, 1)] = (int)b;
+    }
+    __syncthreads();
+    const int nvisit = nocc;
+    __syncthreads();  // nocc read by all before the next screen resets it
+  for (int v = 0; v < nvisit; ++v) {
+    const int b = occ[v];
     const int nb = bin_count[b];
-    if (nb == 0) continue;
     const int s = bin_start[b];
     for (int c = threadIdx.x; c < LOCAL_CELLS; c += blockDim.x) cnt[c] = 0;
     __syncthreads();
@@ -1361,6 +1376,7 @@ __global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_coun
     __syncthreads();
     for (int e = threadIdx.x; e < nb; e += blockDim.x) perm[s + cnt[slc[s + e]] + rk[s + e]] = sidx[s + e];
     __syncthreads();
+  }
   }
 }
 
