@@ -236,7 +236,10 @@ int mpm_get_timing(mpm_ctx *ctx, double *out);
  * default), "split" (1 = stage A + stage B every substep instead of the fused
  * kernel; A/B comparisons), "mega" (1 = substeps 2..L of a stretch as one
  * cooperative kernel with grid barriers between the fused and grid-op
- * phases; pays off for small scenes, e.g. +12% at 30 K particles). */
+ * phases; pays off for small scenes, e.g. +12% at 30 K particles), "pdl"
+ * (1 = fused kernel and grid op launched with programmatic dependent launch,
+ * each kernel's prologue overlapping its predecessor's tail; off by default,
+ * within noise at C3 and -0.4% at C4). */
 int mpm_set_option(mpm_ctx *ctx, const char *key, int value);
 /* Kernel launches issued by this context so far (evidence counter; a graph
  * replay counts every kernel node it runs). */

@@ -829,9 +829,9 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
     TileVel tv0;
     const int4 it0 = p.work[blockIdx.x];
     fused_item_geometry(p, it0, item_box[blockIdx.x], tv0);
-    fused_item_scales(it0, bounds_in[blockIdx.x], scale_s[0]);
     if (dep_wait) griddep_wait();
     fused_item_vtile_issue(p, tv0, vtile);
+    fused_item_scales(it0, bounds_in[blockIdx.x], scale_s[0]);
     cp_async_wait_all();
   } else if (dep_wait) {
     griddep_wait();
