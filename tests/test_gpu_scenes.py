@@ -226,6 +226,22 @@ def test_cooperative_substeps_kernel_matches_per_substep_launches():
         assert rel_l2(a, b) < 1e-5
 
 
+def test_programmatic_dependent_launch_matches_plain_launches():
+    """Option "pdl": fused kernel and grid op launched with programmatic
+    dependent launch (prologue overlapping the predecessor's tail) reproduce
+    the plain stream-ordered launches on the tool-contact scene."""
+    res = {}
+    for pdl in (0, 1):
+        st, mats, params, cols, pose_fn = scenes.c2()
+        sm.step(st, mats, params, cols, pose_fn)
+        st._ctx.call("mpm_set_option", b"pdl", pdl)
+        for _ in range(4):
+            sm.step(st, mats, params, cols, pose_fn)
+        res[pdl] = (st.x.copy(), st.v.copy(), st.F.copy())
+    for a, b in zip(res[0], res[1]):
+        assert rel_l2(a, b) < 1e-5
+
+
 def test_two_materials_match_oracle():
     """Per-particle material ids (SimParams materials list, materials.py:77-82):
     a stiff and a soft block side by side on the floor, 2 frames, against the
