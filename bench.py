@@ -48,6 +48,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "particle-substeps/sec (MLS-MPM, Neo-Hookean)"
 UNIT = "particle-substeps/s"
+NOMINAL_HBM_GBS = 8000.0  # B200 datasheet HBM3e bandwidth (report beside the measured peak)
+GRID_BYTES_PER_NODE = 56   # SURVEY 8d grid term per active node
 BYTES_PER_PARTICLE_SUBSTEP = 200  # fp32 x,v,F,C read+written once + mass,vol0
 
 
@@ -430,6 +432,10 @@ def run_ours(args, rank, world, local_rank):
                      "bytes_per_launch": BYTES_PER_PARTICLE_SUBSTEP * n,
                      "mean_launch_ms": 1000.0 * avg_fused_s, "peak_source": peak_src,
                      "substep_frac": (BYTES_PER_PARTICLE_SUBSTEP * n / substep_s / 1e9) / peak,
+                     "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": achieved / NOMINAL_HBM_GBS,
+                     "grid_bytes_per_launch": GRID_BYTES_PER_NODE * 64 * tbuf[8],
+                     "grid_bytes_note": "SURVEY 8d grid term, 56 B x nodes of the active bricks "
+                                        "(brick-granular: includes massless nodes of active bricks)",
                      "share_of_step": fused_ms / max(prof_ms, 1e-9),
                      "timing": f"mean_launch_ms from a {prof_steps}-frame pass with per-kernel CUDA events "
                                "(value/ms_per_step from the pass without them)"},
@@ -448,11 +454,15 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline and args.config != "c5":
         threads = os.cpu_count() or 1
         rate, times, nn = cpu_oracle_rate(args.config, args.particles, 1, args.cpu_substeps, threads)
+        rate1, times1, _ = cpu_oracle_rate(args.config, args.particles, 1, 1, 1)
+        env_note = (" (one environment: the CPU runs environments one after another, so its "
+                    "particle-substeps/s is the batch's)") if args.config == "c4" else ""
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                "sample": f"{args.cpu_substeps} substeps (after 1 warm-up) of the "
-                                         f"same {args.config} scene, {nn} particles, O1 fp64 C "
+                                         f"same {args.config} scene, {nn} particles{env_note}, O1 fp64 C "
                                          f"restatement of kernels.py, 8 chunks, OpenMP",
-                               "substep_s": times}
+                               "substep_s": times,
+                               "value_1thread": rate1, "substep_s_1thread": times1}
     print(json.dumps(out), flush=True)
 
 
