@@ -38,7 +38,16 @@ __device__ unsigned long long g_fprof[6];
 __device__ unsigned long long g_fcnt[4];  // particles, G2P off-tile, P2G fallback
 __device__ unsigned long long g_gprof[8];  // grid op: sum / max CTA ns, CTAs, launches, sum of per-launch max, clearing launches, bricks
 __device__ unsigned long long g_cprof[4];  // grid contact: warp calls, lanes, cycles, max cycles
-__device__ unsigned long long g_gwin[4] = {~0ull, 0ull, 0ull, 0ull};  // grid op window: min start, max end, sum of windows, max start
+__device__ unsigned long long g_gwin[4] = {~0ull, 0ull, 0ull, 0ull};
+// inter-kernel bubbles: [0] last fused CTA end, [1] last grid-op CTA end, [2] fused min start,
+// [3] fused CTAs done, [4] sum fused->grid gap ns, [5] count, [6] sum grid->fused gap ns, [7] count
+__device__ unsigned long long g_bub[8] = {0ull, 0ull, ~0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+__device__ unsigned long long g_fwin[2];  // fused: sum of (last CTA end - first CTA start), launches
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}  // grid op window: min start, max end, sum of windows, max start
 #define FPROF_COUNT(k) atomicAdd(&g_fcnt[k], 1ull)
 #else
 #define FPROF_COUNT(k)
@@ -982,7 +991,27 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
 __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,
                                                                                   float4* __restrict__ bounds_out,
                                                                                   int* __restrict__ item_box) {
+#ifdef FUSED_PROFILE
+  const unsigned long long t0 = gtimer();
+  if (threadIdx.x == 0) atomicMin(&g_bub[2], t0);
+#endif
   fused_phase(p, bounds_in, bounds_out, item_box, true, true);
+#ifdef FUSED_PROFILE
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&g_bub[0], gtimer());
+    if (atomicAdd(&g_bub[3], 1ull) == gridDim.x - 1) {
+      const unsigned long long st = atomicExch(&g_bub[2], ~0ull), ge = g_bub[1];
+      atomicAdd(&g_fwin[0], gtimer() - st);
+      atomicAdd(&g_fwin[1], 1ull);
+      if (ge && st > ge && st - ge < 50000ull) {
+        atomicAdd(&g_bub[6], st - ge);
+        atomicAdd(&g_bub[7], 1ull);
+      }
+      g_bub[3] = 0;
+    }
+  }
+#endif
 }
 
 // Final G2P of a frame / stage g2p_advect: thread per particle.
@@ -1186,9 +1215,11 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
     unsigned long long g_t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t1));
     if (threadIdx.x == 0) {
-      atomicMin(&g_gwin[0], g_t0);
-      atomicMax(&g_gwin[1], g_t1);
-      atomicMax(&g_gwin[3], g_t0);
+      if (done) {  // window accounting over clearing launches only (reset by their last CTA)
+        atomicMin(&g_gwin[0], g_t0);
+        atomicMax(&g_gwin[1], g_t1);
+        atomicMax(&g_gwin[3], g_t0);
+      }
       atomicAdd(&g_gprof[0], g_t1 - g_t0);
       atomicMax(&g_gprof[1], g_t1 - g_t0);
       atomicAdd(&g_gprof[2], 1ull);
@@ -1208,6 +1239,14 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
         atomicAdd(&g_gprof[4], atomicExch(&g_gprof[1], 0ull));
         atomicAdd(&g_gprof[5], 1ull);
         atomicAdd(&g_gprof[6], (unsigned long long)*p.active_count);
+        {
+          const unsigned long long fe = g_bub[0];
+          if (fe && g_gwin[0] > fe && g_gwin[0] - fe < 50000ull) {  // same substep only
+            atomicAdd(&g_bub[4], g_gwin[0] - fe);
+            atomicAdd(&g_bub[5], 1ull);
+          }
+          atomicMax(&g_bub[1], gtimer());
+        }
         {
           const unsigned long long a = atomicExch(&g_gwin[0], ~0ull), b = atomicExch(&g_gwin[1], 0ull);
           const unsigned long long c = atomicExch(&g_gwin[3], 0ull);

@@ -829,6 +829,13 @@ int mpm_destroy(mpm_ctx* ctx) {
     if (g[5])
       fprintf(stderr, "[grid window] first CTA start -> last CTA end %.2f us, start spread %.2f us (per clearing launch)\n",
               (gw[2] >> 20) / (double)g[5] / 1e3, (gw[2] & ((1ull << 20) - 1)) / (double)g[5] / 1e3);
+    unsigned long long bb[8];
+    cudaMemcpyFromSymbol(bb, g_bub, sizeof(bb));
+    fprintf(stderr, "[bubbles] fused last CTA end -> grid op first CTA start %.2f us (n %llu); grid op end -> fused first start %.2f us (n %llu)\n",
+            bb[4] / (double)(bb[5] ? bb[5] : 1) / 1e3, bb[5], bb[6] / (double)(bb[7] ? bb[7] : 1) / 1e3, bb[7]);
+    unsigned long long fw[2];
+    cudaMemcpyFromSymbol(fw, g_fwin, sizeof(fw));
+    fprintf(stderr, "[fused window] first CTA start -> last CTA end %.2f us (n %llu)\n", fw[0] / (double)(fw[1] ? fw[1] : 1) / 1e3, fw[1]);
     unsigned long long cc[4];
     cudaMemcpyFromSymbol(cc, g_cprof, sizeof(cc));
     if (g[3])
