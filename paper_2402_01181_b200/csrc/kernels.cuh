@@ -47,7 +47,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}  // grid op window: min start, max end, sum of windows, max start
+}
 #define FPROF_COUNT(k) atomicAdd(&g_fcnt[k], 1ull)
 #else
 #define FPROF_COUNT(k)
