@@ -13,4 +13,5 @@ report = sm.step(state, mats, sm.SimParams(), [tool], pose_fn)
 x = state.x
 m = sm.compute_metrics(state, x0)
 mesh = sm.extract_surface(state, iso=300.0)
-print(report, m, len(mesh.vertices), len(mesh.indices))
+frame = sm.encode_surface_frame(state, 300.0, [], 0, 0.0)
+print(report, m, len(mesh.vertices), len(mesh.indices), len(frame))
