@@ -430,7 +430,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic",
         "config": {"workload": workload, "particles_per_gpu": n, "grid": list(st.grid.resolution),
-                   "substeps_per_step": nsub, "parallelism": f"replicas x{world}",
+                   "substeps_per_step": nsub, "parallelism": (f"environment shards x{world}" if args.config == "c4" else f"replicas x{world}"),
                    "l2": "flushed between steps (512 MiB memset)",
                    "wall_s_timed": wall},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -543,14 +543,23 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # plumbing check only (never a measurement): SOFTMPM_BENCH_SHARED_GPU=1 lets
+    # several ranks share the visible GPUs over gloo, to exercise the N > 1 path
+    # (barriers, max over ranks, sharding) on a one-GPU box
+    shared = os.environ.get("SOFTMPM_BENCH_SHARED_GPU") == "1"
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
     if world > 1:
         import torch
         import torch.distributed as tdist
+        if shared:
+            local_rank = local_rank % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if shared:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
