@@ -496,17 +496,23 @@ def run_slab(args, rank, world, local_rank):
     for _ in range(args.warmup):
         slab.step_distributed(win, ex, mats, params)
     n_local = int(_lib_count(win))
+    launches0 = win.state._ctx.launches
     tdist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        slab.step_distributed(win, ex, mats, params)
-    torch.cuda.synchronize()
-    tdist.barrier()
-    el = max_over_ranks(time.perf_counter() - t0, f"cuda:{local_rank}")
+    with ClockSampler(local_rank) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            slab.step_distributed(win, ex, mats, params)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        el_local = time.perf_counter() - t0
+    el = max_over_ranks(el_local, f"cuda:{local_rank}")
     n_total = sum_over_ranks(n_local, f"cuda:{local_rank}")
+    launches = sum_over_ranks(win.state._ctx.launches - launches0, f"cuda:{local_rank}")
     if rank == 0:
         value = n_total * params.substeps_per_frame * args.steps / el
+        peak, peak_src = _peaks()
+        achieved = BYTES_PER_PARTICLE_SUBSTEP * value / world / 1e9
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
@@ -514,7 +520,18 @@ def run_slab(args, rank, world, local_rank):
             "config": {"workload": f"c5: {int(n_total)} particles, {g.resolution[0]}^3 grid, x-slabs over "
                                    f"{world} GPUs ({'peer-memory (IPC/NVLink) halo' if args.exchange == 'ipc' else 'NCCL halo'}"
                                    f" + NCCL migration; wall clock incl. exchanges)",
-                       "parallelism": f"slab x{world}"},
+                       "parallelism": f"slab x{world}",
+                       "timing": "wall clock between device-synchronised barriers (the exchange has host "
+                                 "barriers), max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "kernel": "whole substep per GPU incl. halo exchange and migration (no per-kernel "
+                                   "timing on the slab path)"},
+            "e2e": {"value": None, "unit": UNIT,
+                    "unavailable": "slab path keeps each window's particles on its device between frames; "
+                                   "per-rank host upload/readback is not part of this loop"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
         }), flush=True)
 
 
