@@ -1314,933 +1314,10 @@ __global__ void reset_counter_kernel(int* c, int* c2) {
   if (c2) *c2 = 0;
 }
 
-// ---------------------------------------------------------------------------
-// binning (counting sort by 8^3-cell bin)
-// ---------------------------------------------------------------------------
-
-// Re-binning = counting sort of particle slots by (8^3-cell bin, local cell):
-// bin_key (warp-aggregated counters) -> scan -> bin_fill -> bin_local_sort
-// (per-bin counting sort over the 512 local cells in shared memory) ->
-// gather_permute (coalesced writes).  Lanes of a warp then share cells, so
-// shared-memory tile reads broadcast and int atomics hit few banks.
-__global__ void bin_key_kernel(Params p, int* key, int* lcell, int* rank, int* bin_count) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool valid = i < p.n;
-  const unsigned mask = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return;
-  int c[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    float g = ldf(p, FX + a, i) * p.inv_dx;
-    int bb = (int)floorf(g - 0.5f);
-    c[a] = max(0, min(bb, p.res[a] - 3));
-  }
-  const int k = ((c[0] >> BIN_SHIFT) * p.nbin[1] + (c[1] >> BIN_SHIFT)) * p.nbin[2] + (c[2] >> BIN_SHIFT);
-  key[i] = k;
-  lcell[i] = (((c[0] & (BIN - 1)) * BIN) + (c[1] & (BIN - 1))) * BIN + (c[2] & (BIN - 1));
-  const unsigned peers = __match_any_sync(mask, k);
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(peers) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(bin_count + k, __popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  rank[i] = base + __popc(peers & ((1u << lane) - 1u));
-}
-
-__global__ void bin_fill_kernel(const int* key, const int* lcell, const int* rank, const int* start,
-                                int* sidx, int* slc, long long n) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int d = start[key[i]] + rank[i];
-  sidx[d] = (int)i;
-  slc[d] = lcell[i];
-}
-
-constexpr int LOCAL_CELLS = BIN * BIN * BIN;
-
-// One CTA per bin (grid-stride): counting sort of the bin's slots by local cell.
-// The CTA's bins are screened 256 at a time (one count load per thread) and
-// only the occupied ones visited -- most bins of a sparse scene are empty,
-// and walking them one dependent load at a time dominated the kernel.
-__global__ void __launch_bounds__(256) bin_local_sort_kernel(const int* bin_count, const int* bin_start,
-                                                             int nbins, const int* sidx, const int* slc,
-                                                             int* rk, int* perm, int* bin_maxcnt) {
-  __shared__ int cnt[LOCAL_CELLS];
-  __shared__ int wsum[8];
-  __shared__ int wmax[8];
-  __shared__ int occ[256];
-  __shared__ int nocc;
-  for (long long j0 = 0; (long long)blockIdx.x + j0 * gridDim.x < nbins; j0 += 256) {
-    if (threadIdx.x == 0) nocc = 0;
-    __syncthreads();
-    {
-      const long long b = (long long)blockIdx.x + (j0 + threadIdx.x) * gridDim.x;
-      if (b < nbins && bin_count[b] > 0) occ[atomicAdd(&nocc, 1)] = (int)b;
-    }
-    __syncthreads();
-    const int nvisit = nocc;
-    __syncthreads();  // nocc read by all before the next screen resets it
-  for (int v = 0; v < nvisit; ++v) {
-    const int b = occ[v];
-    const int nb = bin_count[b];
-    const int s = bin_start[b];
-    for (int c = threadIdx.x; c < LOCAL_CELLS; c += blockDim.x) cnt[c] = 0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < nb; e += blockDim.x) rk[s + e] = atomicAdd(&cnt[slc[s + e]], 1);
-    __syncthreads();
-    // exclusive scan of 512 counters: 2 per thread (and the densest cell)
-    const int c0 = cnt[2 * threadIdx.x], c1 = cnt[2 * threadIdx.x + 1];
-    int incl = c0 + c1;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int cm = __reduce_max_sync(0xffffffffu, max(c0, c1));
-    if (lane == 0) wmax[wid] = cm;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    int woff = 0;
-    for (int w = 0; w < wid; ++w) woff += wsum[w];
-    if (threadIdx.x == 0) {
-      int mm = 0;
-      for (int w = 0; w < 8; ++w) mm = max(mm, wmax[w]);
-      bin_maxcnt[b] = mm;
-    }
-    const int excl = woff + incl - c0 - c1;
-    __syncthreads();
-    cnt[2 * threadIdx.x] = excl;
-    cnt[2 * threadIdx.x + 1] = excl + c0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < nb; e += blockDim.x) perm[s + cnt[slc[s + e]] + rk[s + e]] = sidx[s + e];
-    __syncthreads();
-  }
-  }
-}
-
-__global__ void gather_permute_kernel(const float* __restrict__ src, const int* __restrict__ src_mat,
-                                      const int* __restrict__ src_orig, float* __restrict__ dst,
-                                      int* __restrict__ dst_mat, int* __restrict__ dst_orig,
-                                      const int* __restrict__ perm, long long n, long long cap) {
-  const long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (d >= n) return;
-  const long long s = perm[d];
-#pragma unroll
-  for (int f = 0; f < NF; ++f) dst[f * cap + d] = __ldg(src + f * cap + s);
-  dst_mat[d] = __ldg(src_mat + s);
-  dst_orig[d] = __ldg(src_orig + s);
-}
-
-// Work list, sorted by decreasing size class (whole CTA rounds of
-// FUSED_K_THREADS particles) so that the dynamically scheduled kernels hand
-// out the large items first (longest-processing-time order) and finish on
-// the small ones.  Three launches: count per class, class offsets, emit.
-constexpr int WORK_CLASSES = CHUNK / 256 + 2;
-
-__device__ __forceinline__ int work_items_of(int c, int chunk, int& per) {
-  const int items = (c + chunk - 1) / chunk;
-  per = (c + items - 1) / items;  // equal splits (no tiny tail item)
-  return items;
-}
-
-__device__ __forceinline__ int work_class(int size) {
-  return min((size + FUSED_K_THREADS - 1) / FUSED_K_THREADS, WORK_CLASSES - 1);
-}
-
-__global__ void make_work_count_kernel(const int* bin_count, int nbins, int chunk, int* class_count) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nbins) return;
-  const int c = bin_count[b];
-  if (!c) return;
-  int per;
-  const int items = work_items_of(c, chunk, per);
-  for (int t = 0; t < items; ++t) atomicAdd(&class_count[work_class(min(per, c - t * per))], 1);
-}
-
-__global__ void make_work_offsets_kernel(const int* class_count, int* class_cursor, int* nwork) {
-  if (threadIdx.x != 0) return;
-  int s = 0;
-  for (int k = WORK_CLASSES - 1; k >= 0; --k) {
-    class_cursor[k] = s;
-    s += class_count[k];
-  }
-  *nwork = s;
-}
-
-__global__ void make_work_kernel(const int* bin_count, const int* bin_start, const int* bin_maxcnt, int nbins,
-                                 int4* work, int* class_cursor, int chunk) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nbins) return;
-  const int c = bin_count[b];
-  if (!c) return;
-  int per;
-  const int items = work_items_of(c, chunk, per);
-  const int s = bin_start[b];
-  for (int t = 0; t < items; ++t) {
-    const int size = min(per, c - t * per);
-    const int pos = atomicAdd(&class_cursor[work_class(size)], 1);
-    work[pos] = make_int4(b, s + t * per, s + t * per + size, bin_maxcnt[b]);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// exclusive scan (3-phase; 512 threads x 8 items per block)
-// ---------------------------------------------------------------------------
-constexpr int SCAN_THREADS = 512, SCAN_ITEMS = 8, SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
-
-__global__ void __launch_bounds__(SCAN_THREADS) scan_tile_kernel(const int* in, int* out, int* sums,
-                                                                 long long n) {
-  __shared__ int warp_tot[SCAN_THREADS / 32];
-  long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_ITEMS;
-  int v[SCAN_ITEMS];
-  int run = 0;
-#pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    v[q] = base + q < n ? in[base + q] : 0;
-    int t = v[q];
-    v[q] = run;
-    run += t;
-  }
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) warp_tot[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    int t = lane < SCAN_THREADS / 32 ? warp_tot[lane] : 0;
-    int ti = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, ti, o);
-      if (lane >= o) ti += y;
-    }
-    if (lane < SCAN_THREADS / 32) warp_tot[lane] = ti - t;
-    if (lane == SCAN_THREADS / 32 - 1 && sums) sums[blockIdx.x] = ti;
-  }
-  __syncthreads();
-  int off = warp_tot[wid] + incl - run;
-#pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q)
-    if (base + q < n) out[base + q] = v[q] + off;
-}
-
-__global__ void scan_add_kernel(int* out, const int* offs, long long n) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) out[i] += offs[i / SCAN_TILE];
-}
-
-// ---------------------------------------------------------------------------
-// deterministic mode: cell-sorted permutation + node-owner gather
-// ---------------------------------------------------------------------------
-
-__global__ void cell_key_kernel(Params p, int* key, int* rank, int* cell_count) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-  int c[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    float g = __fmul_rn(ldf(p, FX + a, i), p.inv_dx);
-    int bb = (int)floorf(__fsub_rn(g, 0.5f));
-    c[a] = max(0, min(bb, p.res[a] - 3));
-  }
-  int k = (c[0] * p.res[1] + c[1]) * p.res[2] + c[2];
-  key[i] = k;
-  rank[i] = atomicAdd(cell_count + k, 1);
-}
-
-__global__ void cell_fill_kernel(const int* key, const int* rank, const int* start, int* perm,
-                                 long long n) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) perm[start[key[i]] + rank[i]] = (int)i;
-}
-
-// Order each cell's slots by original particle index (insertion sort; cells
-// hold a handful of particles).
-__global__ void cell_sort_kernel(const int* cell_count, const int* start, int* perm, const int* orig,
-                                 long long ncells) {
-  long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (c >= ncells) return;
-  int cnt = cell_count[c];
-  if (cnt < 2) return;
-  int* s = perm + start[c];
-  for (int a = 1; a < cnt; ++a) {
-    int v = s[a], key = orig[v];
-    int b = a - 1;
-    while (b >= 0 && orig[s[b]] > key) {
-      s[b + 1] = s[b];
-      --b;
-    }
-    s[b + 1] = v;
-  }
-}
-
-// payload = (A 9, m v 3) per slot; F advanced in place (exact rounding).
-__global__ void det_payload_kernel(Params p, float* payload) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned inv = 0;
-  if (i < p.n) {
-    float F[9], C[9], A[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      F[q] = ldf(p, FF + q, i);
-      C[q] = ldf(p, FC + q, i);
-    }
-    float m = ldf(p, FMASS, i), vol = ldf(p, FVOL, i);
-    int mid = p.mat[i];
-    float det = affine_update<true>(F, C, m, vol, p.mu[mid], p.lam[mid], p.dt, p.stress_coef,
-                                    p.stress_form, A);
-    inv = det <= 0.0f;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      stf(p, FF + q, i, F[q]);
-      payload[q * p.cap + i] = A[q];
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) payload[(9 + a) * p.cap + i] = __fmul_rn(m, ldf(p, FV + a, i));
-  }
-  warp_count_add(p.inverted, inv);
-}
-
-// Node-owner gather: node (i,j,k) sums its 27 source cells in ascending cell
-// key (offsets 2..0 per axis), particles in ascending original index, from
-// 0.0f with separately rounded ops -- the order of oracle orc32_p2g_sorted.
-__global__ void __launch_bounds__(256) det_gather_kernel(Params p, const float* payload,
-                                                         const int* cell_count, const int* start,
-                                                         const int* perm) {
-  long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long nn = (long long)p.res[0] * p.res[1] * p.res[2];
-  if (node >= nn) return;
-  int gk = (int)(node % p.res[2]);
-  int gj = (int)((node / p.res[2]) % p.res[1]);
-  int gi = (int)(node / ((long long)p.res[1] * p.res[2]));
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int oi = 2; oi >= 0; --oi) {
-    int ci = gi - oi;
-    if (ci < 0 || ci > p.res[0] - 3) continue;
-    for (int oj = 2; oj >= 0; --oj) {
-      int cj = gj - oj;
-      if (cj < 0 || cj > p.res[1] - 3) continue;
-      for (int ok = 2; ok >= 0; --ok) {
-        int ck = gk - ok;
-        if (ck < 0 || ck > p.res[2] - 3) continue;
-        long long cell = ((long long)ci * p.res[1] + cj) * p.res[2] + ck;
-        int s0 = start[cell], s1 = s0 + cell_count[cell];
-        for (int s = s0; s < s1; ++s) {
-          int q = perm[s];
-          int b[3];
-          float f[3], w[3][3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) stencil_rn(ldf(p, FX + a, q), p.inv_dx, p.res[a], b[a], f[a], w[a]);
-          float wt = __fmul_rn(__fmul_rn(w[0][oi], w[1][oj]), w[2][ok]);
-          float dp[3] = {__fmul_rn(__fsub_rn((float)oi, f[0]), p.dx),
-                         __fmul_rn(__fsub_rn((float)oj, f[1]), p.dx),
-                         __fmul_rn(__fsub_rn((float)ok, f[2]), p.dx)};
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            float t = __fadd_rn(payload[(9 + a) * p.cap + q], __fmul_rn(payload[(3 * a) * p.cap + q], dp[0]));
-            t = __fadd_rn(t, __fmul_rn(payload[(3 * a + 1) * p.cap + q], dp[1]));
-            t = __fadd_rn(t, __fmul_rn(payload[(3 * a + 2) * p.cap + q], dp[2]));
-            acc[a] = __fadd_rn(acc[a], __fmul_rn(wt, t));
-          }
-          acc[3] = __fadd_rn(acc[3], __fmul_rn(wt, ldf(p, FMASS, q)));
-        }
-      }
-    }
-  }
-  p.gm[node_index(gi, gj, gk, p.nb[1], p.nb[2])] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-}
-
-// ---------------------------------------------------------------------------
-// host <-> device conversions (fp64 AoS in caller order <-> fp32 SoA slots)
-// ---------------------------------------------------------------------------
-
-// staging layout per particle: x 3, v 3, F 9, C 9 doubles (AoS, caller order)
-__global__ void upload_fields_kernel(Params p, const double* __restrict__ x, const double* __restrict__ v,
-                                     const double* __restrict__ F, const double* __restrict__ C,
-                                     unsigned mask) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
-  long long o = p.orig[s];
-  if (mask & 1u)
-    for (int a = 0; a < 3; ++a) stf(p, FX + a, s, (float)x[3 * o + a]);
-  if (mask & 2u)
-    for (int a = 0; a < 3; ++a) stf(p, FV + a, s, (float)v[3 * o + a]);
-  if (mask & 4u)
-    for (int q = 0; q < 9; ++q) stf(p, FF + q, s, (float)F[9 * o + q]);
-  if (mask & 8u)
-    for (int q = 0; q < 9; ++q) stf(p, FC + q, s, (float)C[9 * o + q]);
-}
-
-__global__ void download_fields_kernel(Params p, double* __restrict__ x, double* __restrict__ v,
-                                       double* __restrict__ F, double* __restrict__ C, unsigned mask) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
-  long long o = p.orig[s];
-  if (mask & 1u)
-    for (int a = 0; a < 3; ++a) x[3 * o + a] = ldf(p, FX + a, s);
-  if (mask & 2u)
-    for (int a = 0; a < 3; ++a) v[3 * o + a] = ldf(p, FV + a, s);
-  if (mask & 4u)
-    for (int q = 0; q < 9; ++q) F[9 * o + q] = ldf(p, FF + q, s);
-  if (mask & 8u)
-    for (int q = 0; q < 9; ++q) C[9 * o + q] = ldf(p, FC + q, s);
-}
-
-__global__ void upload_static_kernel(Params p, const double* mass, const double* vol, const int* mat) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
-  stf(p, FMASS, s, (float)mass[s]);
-  stf(p, FVOL, s, (float)vol[s]);
-  p.mat[s] = mat[s];
-  p.orig[s] = (int)s;
-}
-
-// grid: C-order fp64 (nx,ny,nz,3)+(nx,ny,nz) <-> blocked float4
-__global__ void upload_grid_kernel(Params p, float4* dst, const double* mv, const double* m) {
-  long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long nn = (long long)p.res[0] * p.res[1] * p.res[2];
-  if (node >= nn) return;
-  int gk = (int)(node % p.res[2]);
-  int gj = (int)((node / p.res[2]) % p.res[1]);
-  int gi = (int)(node / ((long long)p.res[1] * p.res[2]));
-  dst[node_index(gi, gj, gk, p.nb[1], p.nb[2])] =
-      make_float4((float)mv[3 * node], (float)mv[3 * node + 1], (float)mv[3 * node + 2],
-                  m ? (float)m[node] : 0.0f);
-}
-
-// phase 0: grid_mv = gm.xyz (after p2g); phase 1: velocity view (after
-// grid_update): massive nodes -> gv, others -> gm.xyz (momentum, untouched
-// by the reference's grid_update).
-__global__ void download_grid_kernel(Params p, int phase, double* mv, double* m) {
-  long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long nn = (long long)p.res[0] * p.res[1] * p.res[2];
-  if (node >= nn) return;
-  int gk = (int)(node % p.res[2]);
-  int gj = (int)((node / p.res[2]) % p.res[1]);
-  int gi = (int)(node / ((long long)p.res[1] * p.res[2]));
-  long long idx = node_index(gi, gj, gk, p.nb[1], p.nb[2]);
-  float4 a = p.gm[idx];
-  float4 o = a;
-  if (phase == 1) {
-    float4 g = p.gv[idx];
-    if (a.w > 0.0f || phase == 2) o = g;
-  } else if (phase == 2) {
-    o = p.gv[idx];
-  }
-  mv[3 * node] = o.x;
-  mv[3 * node + 1] = o.y;
-  mv[3 * node + 2] = o.z;
-  if (m) m[node] = a.w;
-}
-
-__global__ void collision_field_kernel(Params p, Colliders cs, double cap, double* dist, int* obj) {
-  long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long nn = (long long)p.res[0] * p.res[1] * p.res[2];
-  if (node >= nn) return;
-  int gk = (int)(node % p.res[2]);
-  int gj = (int)((node / p.res[2]) % p.res[1]);
-  int gi = (int)(node / ((long long)p.res[1] * p.res[2]));
-  gi += p.goff[0];
-  gj += p.goff[1];
-  gk += p.goff[2];
-  const Colliders ce = env_colliders(cs, gi / p.env_res[0], gj / p.env_res[1], gk / p.env_res[2]);
-  double best;
-  int id = nearest_collider(ce, (double)gi * p.dx64, (double)gj * p.dx64, (double)gk * p.dx64, cap, best);
-  dist[node] = best;
-  obj[node] = id;
-}
-
-__global__ void has_nan_kernel(Params p, int* flag) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
-  bool bad = false;
-  for (int f = 0; f < FC; ++f) bad |= isnan(ldf(p, f, s));
-  if (bad) *flag = 1;
-}
-
-// ---------------------------------------------------------------------------
-// frame-level consumers of the state: metrics and density splat
-// ---------------------------------------------------------------------------
-
-// compute_metrics (scene.py:204-220) without a particle download: per block
-// {lifted count, detached count, sum |det F - 1|, max |x - x0|} in fp64 over
-// a fixed grid-stride partition (block partials are summed on the host in
-// block order).  x0 is in the caller's order, indexed by original id.
-constexpr int METRICS_THREADS = 256;
-
-__global__ void __launch_bounds__(METRICS_THREADS) metrics_kernel(Params p, const double* __restrict__ x0, double dx,
-                                                                  double* __restrict__ part) {
-  double sum = 0.0, mx = 0.0, c_lift = 0.0, c_det = 0.0;
-  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n;
-       s += (long long)gridDim.x * blockDim.x) {
-    const long long id = p.orig[s];
-    const double d0 = (double)ldf(p, FX, s) - x0[3 * id], d1 = (double)ldf(p, FX + 1, s) - x0[3 * id + 1],
-                 d2 = (double)ldf(p, FX + 2, s) - x0[3 * id + 2];
-    c_lift += d1 > 2.0 * dx ? 1.0 : 0.0;
-    c_det += d1 > dx ? 1.0 : 0.0;
-    double F[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) F[q] = (double)ldf(p, FF + q, s);
-    const double det = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
-                       F[2] * (F[3] * F[7] - F[4] * F[6]);
-    sum += fabs(det - 1.0);
-    mx = fmax(mx, sqrt(d0 * d0 + d1 * d1 + d2 * d2));
-  }
-  // fixed-order reduction: warp shuffles, then warps in index order
-  for (int o = 16; o > 0; o >>= 1) {
-    sum += __shfl_down_sync(0xffffffffu, sum, o);
-    c_lift += __shfl_down_sync(0xffffffffu, c_lift, o);
-    c_det += __shfl_down_sync(0xffffffffu, c_det, o);
-    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  }
-  __shared__ double red[METRICS_THREADS / 32][4];
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    red[w][0] = c_lift;
-    red[w][1] = c_det;
-    red[w][2] = sum;
-    red[w][3] = mx;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k = 0; k < METRICS_THREADS / 32; ++k) {
-      r[0] += red[k][0];
-      r[1] += red[k][1];
-      r[2] += red[k][2];
-      r[3] = fmax(r[3], red[k][3]);
-    }
-    for (int k = 0; k < 4; ++k) part[4 * blockIdx.x + k] = r[k];
-  }
-}
-
-// splat_mass (kernels.py:541-576): quadratic B-spline mass deposit on a
-// dense (rx, ry, rz) lattice of spacing 1/inv_dx, C order.  fp64 weights and
-// fp64 atomic accumulation (partition of unity to ~1e-16, so the field
-// integrates to the total mass); the caller scales by 1/dx^3
-// (splat_reduce, kernels.py:579-588).  Source: the context's fp32
-// particles (pos == nullptr) or caller fp64 arrays.  Nodes outside the
-// lattice are skipped (the reference does not bounds-check).
-__global__ void splat_kernel(Params p, const double* __restrict__ pos, const double* __restrict__ mass, long long n,
-                             int rx, int ry, int rz, double inv_dx, double* __restrict__ out) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  double g[3], m;
-  if (pos) {
-    g[0] = pos[3 * s] * inv_dx;
-    g[1] = pos[3 * s + 1] * inv_dx;
-    g[2] = pos[3 * s + 2] * inv_dx;
-    m = mass[s];
-  } else {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) g[a] = (double)ldf(p, FX + a, s) * inv_dx;
-    m = (double)ldf(p, FMASS, s);
-  }
-  int b[3];
-  double w[3][3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    b[a] = (int)floor(g[a] - 0.5);
-    const double f = g[a] - b[a];
-    w[a][0] = 0.5 * ((1.5 - f) * (1.5 - f));
-    w[a][1] = 0.75 - (f - 1.0) * (f - 1.0);
-    w[a][2] = 0.5 * ((f - 0.5) * (f - 0.5));
-  }
-  for (int i = 0; i < 3; ++i) {
-    const int xi = b[0] + i;
-    if (xi < 0 || xi >= rx) continue;
-    for (int j = 0; j < 3; ++j) {
-      const int yj = b[1] + j;
-      if (yj < 0 || yj >= ry) continue;
-      const double wij = w[0][i] * w[1][j];
-      const long long row = ((long long)xi * ry + yj) * rz;
-      for (int k = 0; k < 3; ++k) {
-        const int zk = b[2] + k;
-        if (zk < 0 || zk >= rz) continue;
-        atomicAdd(out + row + zk, wij * w[2][k] * m);
-      }
-    }
-  }
-}
-
-__global__ void scale_kernel(double* v, long long n, double s) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) v[i] *= s;
-}
-
-// Isosurface of a dense (nx, ny, nz) C-order fp64 field (marching cubes,
-// the surfacing step after the splat; surfacing.py:70-95).  Case table:
-// mc_table.h (tools/gen_mc_table.py).  One vertex per crossed lattice edge
-// (edge id = node * 3 + axis, numbered by a scan over the crossing flags), so
-// the mesh is indexed and welded like the reference's; normals are the
-// normalised negative field gradient (central differences, one-sided at the
-// border) interpolated along the edge, i.e. outward from the dense side.
-__device__ __forceinline__ long long mc_node(int i, int j, int k, int ny, int nz) {
-  return ((long long)i * ny + j) * nz + k;
-}
-
-__global__ void mc_edge_flag_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso,
-                                    int* __restrict__ flag) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nn = (long long)nx * ny * nz;
-  if (e >= 3 * nn) return;
-  const long long node = e / 3;
-  const int axis = (int)(e - node * 3);
-  const int k = (int)(node % nz), j = (int)((node / nz) % ny), i = (int)(node / ((long long)ny * nz));
-  const int i2 = i + (axis == 0), j2 = j + (axis == 1), k2 = k + (axis == 2);
-  int c = 0;
-  if (i2 < nx && j2 < ny && k2 < nz) c = (f[node] >= iso) != (f[mc_node(i2, j2, k2, ny, nz)] >= iso);
-  flag[e] = c;
-}
-
-__device__ __forceinline__ void mc_grad(const double* f, int nx, int ny, int nz, int i, int j, int k, double g[3]) {
-  const int ii[3] = {i, j, k}, nn[3] = {nx, ny, nz};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    int lo[3] = {i, j, k}, hi[3] = {i, j, k};
-    lo[a] = max(ii[a] - 1, 0);
-    hi[a] = min(ii[a] + 1, nn[a] - 1);
-    const double span = (double)(hi[a] - lo[a]);
-    g[a] = span > 0.0 ? (f[mc_node(hi[0], hi[1], hi[2], ny, nz)] - f[mc_node(lo[0], lo[1], lo[2], ny, nz)]) / span
-                      : 0.0;
-  }
-}
-
-__global__ void mc_edge_vertex_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso, double dx,
-                                      const int* __restrict__ flag, const int* __restrict__ vid,
-                                      double* __restrict__ verts, double* __restrict__ normals) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nn = (long long)nx * ny * nz;
-  if (e >= 3 * nn || !flag[e]) return;
-  const long long node = e / 3;
-  const int axis = (int)(e - node * 3);
-  const int k = (int)(node % nz), j = (int)((node / nz) % ny), i = (int)(node / ((long long)ny * nz));
-  const int i2 = i + (axis == 0), j2 = j + (axis == 1), k2 = k + (axis == 2);
-  const double f0 = f[node], f1 = f[mc_node(i2, j2, k2, ny, nz)];
-  const double t = (iso - f0) / (f1 - f0);
-  const long long v = vid[e];
-  const double p0[3] = {(double)i, (double)j, (double)k}, p1[3] = {(double)i2, (double)j2, (double)k2};
-  double g0[3], g1[3];
-  mc_grad(f, nx, ny, nz, i, j, k, g0);
-  mc_grad(f, nx, ny, nz, i2, j2, k2, g1);
-  double n[3], nrm = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    verts[3 * v + a] = (p0[a] + t * (p1[a] - p0[a])) * dx;
-    n[a] = -(g0[a] + t * (g1[a] - g0[a]));
-    nrm += n[a] * n[a];
-  }
-  nrm = nrm > 1e-60 ? 1.0 / sqrt(nrm) : 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) normals[3 * v + a] = n[a] * nrm;
-}
-
-__device__ __forceinline__ int mc_case(const double* f, int ny, int nz, int i, int j, int k, double iso) {
-  int c = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int di = (q == 1 || q == 2 || q == 5 || q == 6), dj = (q == 2 || q == 3 || q == 6 || q == 7), dk = q >= 4;
-    c |= (f[mc_node(i + di, j + dj, k + dk, ny, nz)] >= iso) << q;
-  }
-  return c;
-}
-
-__global__ void mc_cell_count_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso,
-                                     int* __restrict__ cnt) {
-  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nc = (long long)(nx - 1) * (ny - 1) * (nz - 1);
-  if (c >= nc) return;
-  const int k = (int)(c % (nz - 1)), j = (int)((c / (nz - 1)) % (ny - 1)), i = (int)(c / ((long long)(ny - 1) * (nz - 1)));
-  cnt[c] = MC_NTRI[mc_case(f, ny, nz, i, j, k, iso)];
-}
-
-__global__ void mc_cell_emit_kernel(const double* __restrict__ f, int nx, int ny, int nz, double iso,
-                                    const int* __restrict__ cnt, const int* __restrict__ off,
-                                    const int* __restrict__ vid, int* __restrict__ tris) {
-  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nc = (long long)(nx - 1) * (ny - 1) * (nz - 1);
-  if (c >= nc || !cnt[c]) return;
-  const int k = (int)(c % (nz - 1)), j = (int)((c / (nz - 1)) % (ny - 1)), i = (int)(c / ((long long)(ny - 1) * (nz - 1)));
-  const int cs = mc_case(f, ny, nz, i, j, k, iso);
-  const int nt = MC_NTRI[cs];
-  const long long o = off[c];
-  for (int q = 0; q < 3 * nt; ++q) {
-    const int e = MC_TRI[cs][q];
-    const int a = MC_EDGE[e][0], b = MC_EDGE[e][1];
-    // lower corner of the edge and its axis
-    const int ca = min(a, b) == a ? a : b;
-    const int ai = (a == 1 || a == 2 || a == 5 || a == 6), aj = (a == 2 || a == 3 || a == 6 || a == 7), ak = a >= 4;
-    const int bi = (b == 1 || b == 2 || b == 5 || b == 6), bj = (b == 2 || b == 3 || b == 6 || b == 7), bk = b >= 4;
-    (void)ca;
-    const int li = min(ai, bi), lj = min(aj, bj), lk = min(ak, bk);
-    const int axis = ai != bi ? 0 : (aj != bj ? 1 : 2);
-    tris[3 * o + q] = vid[mc_node(i + li, j + lj, k + lk, ny, nz) * 3 + axis];
-  }
-}
-
-// MPMF frame body (server.py:65-92) from the device mesh: f32 vertices, f32
-// normals, f32 planar UVs (surfacing.py:92-101: u = clip(x / ext0, 0, 1),
-// v = clip(z / ext2, 0, 1), in fp64 then rounded like numpy's astype) and u32
-// triangle indices, each array contiguous and little-endian, back to back.
-__global__ void mesh_encode_kernel(const double* __restrict__ v, const double* __restrict__ nrm, long long nv,
-                                   const int* __restrict__ tris, long long nt, double ext0, double ext2,
-                                   float* __restrict__ ov, float* __restrict__ on, float* __restrict__ ouv,
-                                   unsigned* __restrict__ ot) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * nv; i += stride) {
-    ov[i] = __double2float_rn(v[i]);
-    on[i] = __double2float_rn(nrm[i]);
-  }
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += stride) {
-    double u = __ddiv_rn(v[3 * i], ext0), w = __ddiv_rn(v[3 * i + 2], ext2);
-    u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
-    w = w < 0.0 ? 0.0 : (w > 1.0 ? 1.0 : w);
-    ouv[2 * i] = __double2float_rn(u);
-    ouv[2 * i + 1] = __double2float_rn(w);
-  }
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * nt; i += stride)
-    ot[i] = (unsigned)tris[i];
-}
-
-// ---------------------------------------------------------------------------
-// slab decomposition (config 5): sparse ghost-brick exchange + migration
-// ---------------------------------------------------------------------------
-
-// Pack the active bricks of one ghost slab (side 0: local x-bricks [0, gb),
-// side 1: [nb0 - gb, nb0)) as records {global brick id, 64 x float4 gm}.
-// rec_ids/rec_data: capacity-sized buffers; *count receives the record count.
-__global__ void halo_pack_kernel(Params p, int side, int gb, int* rec_ids, float4* rec_data, int* count) {
-  const int nitems = *p.active_count;
-  const int lane = threadIdx.x & 31;
-  for (int it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems;
-       it += gridDim.x * (blockDim.x >> 5)) {
-    const int b = p.active_list[it];
-    const int bi = b / (p.nb[1] * p.nb[2]);
-    const bool ghost = side == 0 ? bi < gb : bi >= p.nb[0] - gb;
-    if (!ghost) continue;
-    int slot = 0;
-    if (lane == 0) slot = atomicAdd(count, 1);
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    if (lane == 0) {
-      const int rem = b - bi * (p.nb[1] * p.nb[2]);
-      rec_ids[slot] = (bi + (p.goff[0] >> BRICK_SHIFT)) * (p.nb[1] * p.nb[2]) + rem;  // global brick id
-    }
-    rec_data[(long long)slot * 64 + lane] = p.gm[((long long)b << 6) + lane];
-    rec_data[(long long)slot * 64 + lane + 32] = p.gm[((long long)b << 6) + lane + 32];
-  }
-}
-
-// Add received ghost records into the owned bricks (global -> local brick id)
-// and mark them active; remembers the local ids for the velocity reply.
-__global__ void halo_unpack_add_kernel(Params p, const int* rec_ids, const float4* rec_data, int n, int* local_ids) {
-  const int lane = threadIdx.x & 31;
-  const int per_slab = p.nb[1] * p.nb[2];
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
-    const int gbid = rec_ids[r];
-    const int b = gbid - (p.goff[0] >> BRICK_SHIFT) * per_slab;
-    if (lane == 0) local_ids[r] = b;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const long long idx = ((long long)b << 6) + lane + 32 * h;
-      const float4 a = rec_data[(long long)r * 64 + lane + 32 * h];
-      float4 g = p.gm[idx];
-      g.x += a.x;
-      g.y += a.y;
-      g.z += a.z;
-      g.w += a.w;
-      p.gm[idx] = g;
-    }
-    if (lane == 0) mark_brick(p, (long long)b << 6);
-  }
-}
-
-// Velocity reply: gv of the bricks received from a side, in receive order.
-__global__ void halo_pack_vel_kernel(Params p, const int* local_ids, int n, float4* rec_data) {
-  const int lane = threadIdx.x & 31;
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
-    const long long b = local_ids[r];
-    rec_data[(long long)r * 64 + lane] = p.gv[(b << 6) + lane];
-    rec_data[(long long)r * 64 + lane + 32] = p.gv[(b << 6) + lane + 32];
-  }
-}
-
-// Write the owner's velocities into our ghost bricks (ids = our packed global ids).
-__global__ void halo_unpack_vel_kernel(Params p, const int* rec_ids, const float4* rec_data, int n) {
-  const int lane = threadIdx.x & 31;
-  const int per_slab = p.nb[1] * p.nb[2];
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
-    const long long b = rec_ids[r] - (p.goff[0] >> BRICK_SHIFT) * per_slab;
-    p.gv[(b << 6) + lane] = rec_data[(long long)r * 64 + lane];
-    p.gv[(b << 6) + lane + 32] = rec_data[(long long)r * 64 + lane + 32];
-  }
-}
-
-// ---- peer-memory halo exchange (CUDA IPC / NVLink P2P) ------------------
-// The pack kernels write straight into the NEIGHBOUR's receive buffers
-// (mapped with cudaIpcOpenMemHandle; P2P stores and atomics over NVLink
-// between GPUs), so packing and the transfer are one kernel; record counts
-// live on the device and never visit the host.
-
-// Ghost bricks of one side -> the neighbour's receive buffers; slot from the
-// neighbour's counter, the global ids also kept locally for the velocity reply.
-__global__ void ipc_pack_kernel(Params p, int side, int gb, int* peer_ids, float4* peer_data, int* peer_count,
-                                int* my_ids, int* my_sent) {
-  const int nitems = *p.active_count;
-  const int lane = threadIdx.x & 31;
-  for (int it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems;
-       it += gridDim.x * (blockDim.x >> 5)) {
-    const int b = p.active_list[it];
-    const int bi = b / (p.nb[1] * p.nb[2]);
-    const bool ghost = side == 0 ? bi < gb : bi >= p.nb[0] - gb;
-    if (!ghost) continue;
-    int slot = 0;
-    if (lane == 0) slot = atomicAdd(peer_count, 1);
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    if (lane == 0) {
-      const int rem = b - bi * (p.nb[1] * p.nb[2]);
-      const int gbid = (bi + (p.goff[0] >> BRICK_SHIFT)) * (p.nb[1] * p.nb[2]) + rem;
-      peer_ids[slot] = gbid;
-      my_ids[slot] = gbid;
-      atomicMax(my_sent, slot + 1);
-    }
-    peer_data[(long long)slot * 64 + lane] = p.gm[((long long)b << 6) + lane];
-    peer_data[(long long)slot * 64 + lane + 32] = p.gm[((long long)b << 6) + lane + 32];
-  }
-}
-
-__global__ void ipc_unpack_add_kernel(Params p, const int* rec_ids, const float4* rec_data, const int* count,
-                                      int* local_ids) {
-  const int n = *count;
-  const int lane = threadIdx.x & 31;
-  const int per_slab = p.nb[1] * p.nb[2];
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
-    const int b = rec_ids[r] - (p.goff[0] >> BRICK_SHIFT) * per_slab;
-    if (lane == 0) local_ids[r] = b;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const long long idx = ((long long)b << 6) + lane + 32 * h;
-      const float4 a = rec_data[(long long)r * 64 + lane + 32 * h];
-      float4 g = p.gm[idx];
-      g.x += a.x;
-      g.y += a.y;
-      g.z += a.z;
-      g.w += a.w;
-      p.gm[idx] = g;
-    }
-    if (lane == 0) mark_brick(p, (long long)b << 6);
-  }
-}
-
-// Velocity reply straight into the neighbour's velocity receive buffer.
-__global__ void ipc_pack_vel_kernel(Params p, const int* local_ids, const int* n_recv, float4* peer_vdata) {
-  const int n = *n_recv;
-  const int lane = threadIdx.x & 31;
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
-    const long long b = local_ids[r];
-    peer_vdata[(long long)r * 64 + lane] = p.gv[(b << 6) + lane];
-    peer_vdata[(long long)r * 64 + lane + 32] = p.gv[(b << 6) + lane + 32];
-  }
-}
-
-__global__ void ipc_unpack_vel_kernel(Params p, const int* my_ids, const int* my_sent, const float4* vdata) {
-  const int n = *my_sent;
-  const int lane = threadIdx.x & 31;
-  const int per_slab = p.nb[1] * p.nb[2];
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
-    const long long b = my_ids[r] - (p.goff[0] >> BRICK_SHIFT) * per_slab;
-    p.gv[(b << 6) + lane] = vdata[(long long)r * 64 + lane];
-    p.gv[(b << 6) + lane + 32] = vdata[(long long)r * 64 + lane + 32];
-  }
-}
-
-// Migration: flag = 0 keep, 1 leaves to the low neighbour, 2 to the high one
-// (global base cell x outside [own_lo, own_hi)).
-__global__ void migrant_flag_kernel(Params p, int own_lo, int own_hi, int* flag) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-  const float g = (ldf(p, FX, i) + p.goffx[0]) * p.inv_dx;
-  const int b = (int)floorf(g - 0.5f);
-  flag[i] = b < own_lo ? 1 : (b >= own_hi ? 2 : 0);
-}
-
-// Stable compaction by flag class via exclusive scans: dst row = pos[class][i].
-__global__ void migrant_scatter_kernel(Params p, const int* flag, const int* pos_keep, const int* pos_lo,
-                                       const int* pos_hi, float* keep_P, int* keep_mat, int* keep_orig,
-                                       float* out_lo, float* out_hi, long long out_cap) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-  const int f = flag[i];
-  if (f == 0) {
-    const long long d = pos_keep[i];
-#pragma unroll
-    for (int q = 0; q < NF; ++q) keep_P[q * p.cap + d] = ldf(p, q, i);
-    keep_mat[d] = p.mat[i];
-    keep_orig[d] = p.orig[i];
-  } else {
-    // row layout: NF floats, mat, orig (as float bits)
-    float* out = f == 1 ? out_lo : out_hi;
-    const long long d = f == 1 ? pos_lo[i] : pos_hi[i];
-#pragma unroll
-    for (int q = 0; q < NF; ++q) out[q * out_cap + d] = ldf(p, q, i);
-    out[NF * out_cap + d] = __int_as_float(p.mat[i]);
-    out[(NF + 1) * out_cap + d] = __int_as_float(p.orig[i]);
-  }
-}
-
-__global__ void flag_class_kernel(const int* flag, int cls, int* out, long long n) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = flag[i] == cls;
-}
-
-// Append m migrant rows (row layout of migrant_scatter_kernel) at slot n0,
-// shifting x by dxs (source window offset - ours, in metres).
-__global__ void append_rows_kernel(Params p, const float* rows, long long m, long long rows_cap, long long n0,
-                                   float dxs) {
-  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  const long long d = n0 + r;
-#pragma unroll
-  for (int q = 0; q < NF; ++q) {
-    float v = rows[q * rows_cap + r];
-    if (q == FX) v += dxs;
-    p.P[q * p.cap + d] = v;
-  }
-  p.mat[d] = __float_as_int(rows[NF * rows_cap + r]);
-  p.orig[d] = __float_as_int(rows[(NF + 1) * rows_cap + r]);
-}
-
-__global__ void set_ids_kernel(Params p, const int* ids) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s < p.n) p.orig[s] = ids[p.orig[s]];
-}
-
-// x (global), v, F, C in device order (slab windows: rows are identified by id).
-__global__ void download_rows_kernel(Params p, double* x, double* v, double* F, double* C) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    x[3 * s + a] = (double)ldf(p, FX + a, s) + (double)p.goffx[a];
-    v[3 * s + a] = ldf(p, FV + a, s);
-  }
-#pragma unroll
-  for (int q = 0; q < 9; ++q) {
-    F[9 * s + q] = ldf(p, FF + q, s);
-    C[9 * s + q] = ldf(p, FC + q, s);
-  }
-}
-
-__global__ void download_ids_kernel(Params p, int* ids, double* x) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
-  ids[s] = p.orig[s];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) x[3 * s + a] = (double)ldf(p, FX + a, s) + (double)p.goffx[a];
-}
-
 }  // namespace mpm
+
+#include "binning.cuh"
+#include "determinism.cuh"
+#include "conversions.cuh"
+#include "frame_ops.cuh"
+#include "slab_halo.cuh"
