@@ -143,6 +143,12 @@ int64_t mpm_ipc_blob_size(void);
 int mpm_ipc_export(mpm_ctx *ctx, int side, void *blob);
 int mpm_ipc_import(mpm_ctx *ctx, int side, const void *peer_blob);
 int mpm_ipc_halo(mpm_ctx *ctx, int phase, int sides);
+/* 1 when mpm_ipc_halo orders the neighbours' streams by itself (stream
+ * memory operations: a wait on our counter, a write into the neighbour's,
+ * no host barrier per substep); 0 on the interprocess-event fallback
+ * (SOFTMPM_IPC_EVENTS set, or no driver entry points), where the caller
+ * barriers between phases 0/1 and 2/3. */
+int mpm_ipc_mode(mpm_ctx *ctx, int *device_ordered);
 
 /* ---- slab decomposition (BASELINE config 5) ------------------------------
  * A context can own an x-window of a larger global grid: its res[0] nodes

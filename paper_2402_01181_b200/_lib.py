@@ -39,7 +39,7 @@ EXPORTS = (
     "mpm_halo_unpack_add", "mpm_halo_pack_vel", "mpm_halo_unpack_vel", "mpm_extract_migrants",
     "mpm_append_particles", "mpm_reserve", "mpm_download_ids", "mpm_device_copy", "mpm_set_ids",
     "mpm_download_rows", "mpm_metrics", "mpm_splat_density", "mpm_splat_density_host",
-    "mpm_marching_cubes", "mpm_mesh_fetch", "mpm_mesh_encode", "mpm_ipc_blob_size", "mpm_ipc_export", "mpm_ipc_import",
+    "mpm_marching_cubes", "mpm_mesh_fetch", "mpm_mesh_encode", "mpm_ipc_blob_size", "mpm_ipc_export", "mpm_ipc_import", "mpm_ipc_mode",
     "mpm_ipc_halo",
 )
 
@@ -131,6 +131,7 @@ def lib():
     L.mpm_ipc_export.argtypes = [_VP, ctypes.c_int, ctypes.c_char_p]
     L.mpm_ipc_import.argtypes = [_VP, ctypes.c_int, ctypes.c_char_p]
     L.mpm_ipc_halo.argtypes = [_VP, ctypes.c_int, ctypes.c_int]
+    L.mpm_ipc_mode.argtypes = [_VP, ctypes.POINTER(ctypes.c_int)]
     _lib = L
     return L
 

@@ -5,6 +5,7 @@
 // particles binned (8^3-cell bins, counting sort) and runs each stretch of
 // substeps as  rebin -> P2G -> [grid op -> fused G2P/P2G] x (L-1) -> grid op
 // -> G2P, with only active bricks visited on the grid.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -136,6 +137,9 @@ struct mpm_ctx {
   int* peer_cnt[2] = {nullptr, nullptr};
   float4* peer_vdata[2] = {nullptr, nullptr};
   cudaEvent_t peer_free[2] = {nullptr, nullptr}, peer_ready[2] = {nullptr, nullptr};
+  // stream-memory-op protocol (no host barriers): per side, writes into the
+  // neighbour's buffers done / the neighbour's writes consumed
+  unsigned ipc_writes[2] = {0, 0}, ipc_reads[2] = {0, 0};
   int stage_nsub = 0, stage_col = 0;
   // migration scratch
   int* mflag = nullptr;
@@ -1658,8 +1662,8 @@ int mpm_ipc_export(mpm_ctx* ctx, int side, void* out) {
   CK(cudaSetDevice(ctx->dev));
   if (!ctx->ipc_vrecv[side]) {
     TRY(dalloc(ctx, &ctx->ipc_vrecv[side], (size_t)(ctx->h_cap + 1) * 64));
-    TRY(dalloc(ctx, &ctx->ipc_cnt[side], 4));
-    CK(cudaMemset(ctx->ipc_cnt[side], 0, 4 * sizeof(int)));
+    TRY(dalloc(ctx, &ctx->ipc_cnt[side], 8));
+    CK(cudaMemset(ctx->ipc_cnt[side], 0, 8 * sizeof(int)));
     CK(cudaEventCreateWithFlags(&ctx->ipc_free[side], cudaEventInterprocess | cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ipc_ready[side], cudaEventInterprocess | cudaEventDisableTiming));
   }
@@ -1700,46 +1704,120 @@ int mpm_ipc_import(mpm_ctx* ctx, int side, const void* peer) {
 
 int64_t mpm_ipc_blob_size(void) { return (int64_t)IPC_BLOB; }
 
+// Stream memory operations (driver entry points through the runtime): the
+// halo protocol orders the neighbours' streams with counters in device memory
+// -- a wait on our own counter, a write into the neighbour's (IPC-mapped,
+// NVLink between GPUs) -- so no host barrier is needed per substep.
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamWaitValue32Fn stream_wait_value32() {
+  static StreamWaitValue32Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<StreamWaitValue32Fn>(f);
+  }();
+  return fn;
+}
+static StreamWriteValue32Fn stream_write_value32() {
+  static StreamWriteValue32Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<StreamWriteValue32Fn>(f);
+  }();
+  return fn;
+}
+
+int mpm_ipc_mode(mpm_ctx* ctx, int* device_ordered) {
+  if (!ctx || !device_ordered) return MPM_EINVAL;
+  *device_ordered = stream_wait_value32() && stream_write_value32() && !getenv("SOFTMPM_IPC_EVENTS") ? 1 : 0;
+  return 0;
+}
+
+// Wait until our counter cnt[k] reaches v / set the neighbour's counter to v.
+static int ipc_wait(mpm_ctx* ctx, int* cnt, int k, unsigned v) {
+  if (stream_wait_value32()(reinterpret_cast<CUstream>(ctx->stream), reinterpret_cast<CUdeviceptr>(cnt + k), v,
+                            CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return fail(ctx, MPM_ECUDA, "ipc_halo: stream wait failed");
+  return 0;
+}
+static int ipc_signal(mpm_ctx* ctx, int* peer_cnt, int k, unsigned v) {
+  if (stream_write_value32()(reinterpret_cast<CUstream>(ctx->stream), reinterpret_cast<CUdeviceptr>(peer_cnt + k), v,
+                             CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    return fail(ctx, MPM_ECUDA, "ipc_halo: stream write failed");
+  return 0;
+}
+
 int mpm_ipc_halo(mpm_ctx* ctx, int phase, int sides) {
   if (!ctx || phase < 0 || phase > 3) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
+  int ordered = 0;
+  TRY(mpm_ipc_mode(ctx, &ordered));
   Params p = make_params(ctx);
   for (int sd = 0; sd < 2; ++sd) {
     if (!((sides >> sd) & 1)) continue;
     if (!ctx->peer_ids[sd] || !ctx->ipc_cnt[sd]) return fail(ctx, MPM_ESTATE, "ipc_halo: side not connected");
-    int* cnt = ctx->ipc_cnt[sd];  // [0] records received, [1] received last, [2] records sent
+    // [0] records received, [1] received last, [2] records sent,
+    // [4] neighbour's writes ready (set by it), [5] our writes consumed (set by it)
+    int* cnt = ctx->ipc_cnt[sd];
+    int* pcnt = ctx->peer_cnt[sd];
+    // before writing into the neighbour: it consumed our previous write
+    auto before_write = [&]() -> int {
+      if (ordered) return ipc_wait(ctx, cnt, 5, ctx->ipc_writes[sd]);
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_free[sd], 0));
+      return 0;
+    };
+    auto after_write = [&]() -> int {
+      if (ordered) return ipc_signal(ctx, pcnt, 4, ++ctx->ipc_writes[sd]);
+      CK(cudaEventRecord(ctx->ipc_ready[sd], ctx->stream));
+      return 0;
+    };
+    auto before_read = [&]() -> int {
+      if (ordered) return ipc_wait(ctx, cnt, 4, ++ctx->ipc_reads[sd]);
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_ready[sd], 0));
+      return 0;
+    };
+    auto after_read = [&]() -> int {
+      if (ordered) return ipc_signal(ctx, pcnt, 5, ctx->ipc_reads[sd]);
+      CK(cudaEventRecord(ctx->ipc_free[sd], ctx->stream));
+      return 0;
+    };
     switch (phase) {
       case 0:  // ghost momentum -> neighbour (after it consumed our last writes)
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_free[sd], 0));
+        TRY(before_write());
         ipc_pack_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, sd, ctx->ghost_bricks, ctx->peer_ids[sd],
-                                                               ctx->peer_data[sd], ctx->peer_cnt[sd],
-                                                               ctx->h_send_ids[sd], cnt + 2);
+                                                               ctx->peer_data[sd], pcnt, ctx->h_send_ids[sd], cnt + 2);
         LAUNCHED();
-        CK(cudaEventRecord(ctx->ipc_ready[sd], ctx->stream));
+        TRY(after_write());
         break;
       case 1:  // add the neighbour's ghost momentum into our owned bricks
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_ready[sd], 0));
+        TRY(before_read());
         ipc_unpack_add_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_recv_ids[sd], ctx->h_recv_data[sd], cnt,
                                                                      ctx->h_local_ids[sd]);
         LAUNCHED();
         CK(cudaMemcpyAsync(cnt + 1, cnt, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
         CK(cudaMemsetAsync(cnt, 0, sizeof(int), ctx->stream));
-        CK(cudaEventRecord(ctx->ipc_free[sd], ctx->stream));
+        TRY(after_read());
         break;
       case 2:  // velocities of the received bricks -> neighbour
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_free[sd], 0));
+        TRY(before_write());
         ipc_pack_vel_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_local_ids[sd], cnt + 1,
                                                                    ctx->peer_vdata[sd]);
         LAUNCHED();
-        CK(cudaEventRecord(ctx->ipc_ready[sd], ctx->stream));
+        TRY(after_write());
         break;
       case 3:  // the owner's velocities into our ghost bricks
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_ready[sd], 0));
+        TRY(before_read());
         ipc_unpack_vel_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(p, ctx->h_send_ids[sd], cnt + 2,
                                                                      ctx->ipc_vrecv[sd]);
         LAUNCHED();
         CK(cudaMemsetAsync(cnt + 2, 0, sizeof(int), ctx->stream));
-        CK(cudaEventRecord(ctx->ipc_free[sd], ctx->stream));
+        TRY(after_read());
         break;
     }
   }

@@ -196,15 +196,18 @@ class TorchExchange:
 
 class IpcExchange:
     """Peer-memory halo exchange between neighbouring ranks: each window maps
-    its neighbours' receive buffers and events (CUDA IPC; NVLink P2P between
-    GPUs) and the pack kernels write straight into them (mpm_ipc_halo), so
-    per substep only two host barriers remain.  Migration at re-binning and
-    the one-time handle exchange go through torch.distributed."""
+    its neighbours' receive buffers (CUDA IPC; NVLink P2P between GPUs) and
+    the pack kernels write straight into them (mpm_ipc_halo); the streams are
+    ordered by counters in device memory (stream wait / write-value
+    operations), so a substep has no host barrier (interprocess events plus
+    two host barriers per substep remain as the fallback).  Migration at
+    re-binning and the one-time handle exchange go through torch.distributed."""
 
     def __init__(self, window, rank, world, device="cuda"):
         self.host = TorchExchange(window, rank, world, device)
         self.win, self.rank, self.world, self.device = window, rank, world, device
         self.sides = None
+        self.device_ordered = False
 
     def connect(self, ctx):
         """Export our buffers / events, map the neighbours' (collective: every
@@ -225,6 +228,12 @@ class IpcExchange:
         for side, nb in _neighbours(self.rank, self.world).items():
             ctx.call("mpm_ipc_import", side, every[nb][1 - side])
             self.sides |= 1 << side
+        mode = ctypes.c_int(0)
+        ctx.call("mpm_ipc_mode", ctypes.byref(mode))
+        # every rank must agree (a mixed pair would deadlock)
+        modes = [None] * self.world
+        dist.all_gather_object(modes, int(mode.value))
+        self.device_ordered = all(m == 1 for m in modes)
         dist.barrier()
 
     def counts(self, mine):
@@ -383,11 +392,13 @@ def step_distributed(win: SlabWindow, ex, materials, params, colliders=None, pos
             if isinstance(ex, IpcExchange):
                 import torch.distributed as dist
                 ex.halo(ctx, 0)
-                dist.barrier()
+                if not ex.device_ordered:
+                    dist.barrier()  # event fallback: records before the matching waits
                 ex.halo(ctx, 1)
                 ctx.call("mpm_stage_grid", sub, int(sub != nsub - 1))
                 ex.halo(ctx, 2)
-                dist.barrier()
+                if not ex.device_ordered:
+                    dist.barrier()
                 ex.halo(ctx, 3)
                 continue
             counts = {}

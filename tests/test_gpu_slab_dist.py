@@ -49,6 +49,8 @@ def _worker(rank, world, port, out_dir, kind):
             assert ex.host_staging
         for _ in range(FRAMES):
             slab.step_distributed(win, ex, mats, params)
+        if kind == "ipc":  # stream-memory-op ordering unless the event fallback is forced
+            assert ex.device_ordered == (os.environ.get("SOFTMPM_IPC_EVENTS") is None)
         ids, xw, vw, Fw, _ = win.download()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=ids, x=xw, v=vw, F=Fw)
     finally:
