@@ -521,8 +521,8 @@ def run_slab(args, rank, world, local_rank):
                                    f"{world} GPUs ({'peer-memory (IPC/NVLink) halo' if args.exchange == 'ipc' else 'NCCL halo'}"
                                    f" + NCCL migration; wall clock incl. exchanges)",
                        "parallelism": f"slab x{world}",
-                       "timing": "wall clock between device-synchronised barriers (the exchange has host "
-                                 "barriers), max over ranks"},
+                       "timing": "wall clock between device-synchronised barriers around the timed frames "
+                                 "(migration syncs the host once per stretch), max over ranks"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_source": peak_src,
                          "kernel": "whole substep per GPU incl. halo exchange and migration (no per-kernel "
