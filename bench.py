@@ -308,10 +308,10 @@ def run_ours(args, rank, world, local_rank):
     ctx = st._ctx
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
 
-    def frame():
+    def frame(rows=None):
         t0 = batch.time if batch is not None else st.time
         if cols:
-            st._upload_pose_rows(*rows_for(t0))
+            st._upload_pose_rows(*(rows if rows is not None else rows_for(t0)))
         inv = ctypes.c_int64(0)
         ms = ctypes.c_double(0.0)
         ctx.call("mpm_substeps", nsub, int(bool(cols)), ctypes.byref(inv), ctypes.byref(ms))
@@ -402,9 +402,16 @@ def run_ours(args, rank, world, local_rank):
         tdist.barrier()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
+    import threading
     for _ in range(e2e_steps):
-        ctx.call("mpm_upload_fields", ctypes.c_uint32(15), *[_lib.ptr(host[k]) for k in sizes])
-        frame()
+        # as core.step does: the field upload on a worker thread (the copy
+        # releases the GIL) while this thread builds the frame's pose table
+        up = threading.Thread(target=ctx.call, args=("mpm_upload_fields", ctypes.c_uint32(15),
+                                                     *[_lib.ptr(host[k]) for k in sizes]))
+        up.start()
+        rows = rows_for(batch.time if batch is not None else st.time) if cols else None
+        up.join()
+        frame(rows)
         ctx.call("mpm_download_particles", ctypes.c_uint32(15), *[_lib.ptr(host[k]) for k in sizes])
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - e0

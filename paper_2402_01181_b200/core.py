@@ -508,6 +508,29 @@ def _run_substeps(state: SimState, materials, params: SimParams, colliders, nsub
     return int(inv.value), float(dev_ms.value)
 
 
+class _Upload:
+    """SimState._prepare (context config, materials, host-dirty field upload)
+    on a worker thread; join() re-raises its error on the caller's thread."""
+
+    def __init__(self, state, materials, params, theta):
+        import threading
+        self.err = None
+
+        def run():
+            try:
+                state._prepare(materials, params, theta)
+            except BaseException as e:  # noqa: BLE001 -- handed to the caller
+                self.err = e
+
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+
+    def join(self):
+        self.t.join()
+        if self.err is not None:
+            raise self.err
+
+
 def substep(state: SimState, materials: list[Material], params: SimParams,
             colliders: list[RigidCollider] | None = None) -> int:
     """One substep (core.py:261-277); returns the inverted-element count."""
@@ -564,6 +587,12 @@ def step(state: SimState, materials: list[Material], params: SimParams,
     nsub = params.substeps_per_frame
     t_collision = 0.0
     rows = None
+    upload = None
+    if colliders and state._ctx is not None and state._host_dirty and not state._static_dirty:
+        # host-modified fields go up on a worker thread (the copy releases the
+        # GIL) while this thread builds the frame's pose table; pose_fn itself
+        # stays on the caller's thread
+        upload = _Upload(state, materials, params, _theta(state, params))
     if colliders:
         t0 = _time.perf_counter()
         if pose_fn is not None:
@@ -572,6 +601,8 @@ def step(state: SimState, materials: list[Material], params: SimParams,
             rows = _pose_arrays(state._packed_colliders(colliders, params))
         t_collision += _time.perf_counter() - t0
     t0 = _time.perf_counter()
+    if upload is not None:
+        upload.join()
     inv, _ = _run_substeps(state, materials, params, colliders, nsub, rows)
     t_soft = _time.perf_counter() - t0
     for _ in range(nsub):
