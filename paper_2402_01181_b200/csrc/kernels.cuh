@@ -42,7 +42,7 @@ __device__ unsigned long long g_gwin[4] = {~0ull, 0ull, 0ull, 0ull};
 // inter-kernel bubbles: [0] last fused CTA end, [1] last grid-op CTA end, [2] fused min start,
 // [3] fused CTAs done, [4] sum fused->grid gap ns, [5] count, [6] sum grid->fused gap ns, [7] count
 __device__ unsigned long long g_bub[8] = {0ull, 0ull, ~0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
-__device__ unsigned long long g_fwin[2];  // fused: sum of (last CTA end - first CTA start), launches
+__device__ unsigned long long g_fwin[4];  // fused: sum of windows, launches, sum of CTA durations, CTAs
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -999,7 +999,10 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
 #ifdef FUSED_PROFILE
   __syncthreads();
   if (threadIdx.x == 0) {
-    atomicMax(&g_bub[0], gtimer());
+    const unsigned long long t_end = gtimer();
+    atomicAdd(&g_fwin[2], t_end - t0);
+    atomicAdd(&g_fwin[3], 1ull);
+    atomicMax(&g_bub[0], t_end);
     if (atomicAdd(&g_bub[3], 1ull) == gridDim.x - 1) {
       const unsigned long long st = atomicExch(&g_bub[2], ~0ull), ge = g_bub[1];
       atomicAdd(&g_fwin[0], gtimer() - st);

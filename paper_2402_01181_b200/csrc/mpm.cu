@@ -837,9 +837,10 @@ int mpm_destroy(mpm_ctx* ctx) {
     cudaMemcpyFromSymbol(bb, g_bub, sizeof(bb));
     fprintf(stderr, "[bubbles] fused last CTA end -> grid op first CTA start %.2f us (n %llu); grid op end -> fused first start %.2f us (n %llu)\n",
             bb[4] / (double)(bb[5] ? bb[5] : 1) / 1e3, bb[5], bb[6] / (double)(bb[7] ? bb[7] : 1) / 1e3, bb[7]);
-    unsigned long long fw[2];
+    unsigned long long fw[4];
     cudaMemcpyFromSymbol(fw, g_fwin, sizeof(fw));
-    fprintf(stderr, "[fused window] first CTA start -> last CTA end %.2f us (n %llu)\n", fw[0] / (double)(fw[1] ? fw[1] : 1) / 1e3, fw[1]);
+    fprintf(stderr, "[fused window] first CTA start -> last CTA end %.2f us (n %llu), mean CTA duration %.2f us\n",
+            fw[0] / (double)(fw[1] ? fw[1] : 1) / 1e3, fw[1], fw[2] / (double)(fw[3] ? fw[3] : 1) / 1e3);
     unsigned long long cc[4];
     cudaMemcpyFromSymbol(cc, g_cprof, sizeof(cc));
     if (g[3])
