@@ -114,7 +114,7 @@ struct GlobalVel {
 };
 
 struct TileVel {
-  const float* t;  // 3 x TILE_NODES floats (vx | vy | vz)
+  const float* t;  // 3 x TILE_NODES floats: (vx, vy) pairs, then vz
   int org[3];
   int lo[3], hi[3];  // loaded base-cell box (tile coords); nodes [lo, hi + 2]
   __device__ __forceinline__ void offsets(const int b[3], int ox[3], int oy[3], int oz[3]) const {
@@ -126,7 +126,8 @@ struct TileVel {
     }
   }
   __device__ __forceinline__ float3 load(int idx) const {
-    return make_float3(t[idx], t[TILE_NODES + idx], t[2 * TILE_NODES + idx]);
+    const float2 xy = reinterpret_cast<const float2*>(t)[idx];
+    return make_float3(xy.x, xy.y, t[2 * TILE_NODES + idx]);
   }
 };
 
@@ -422,8 +423,7 @@ __device__ __forceinline__ void load_vtile_column(const Params& p, float* vtile,
     for (int u = 0; u < G; ++u) {
       if (xs + u <= x1) {
         const int t = ((xs + u) * TILE + ty) * TILE_Z + tz;
-        vtile[t] = g[u].x;
-        vtile[TILE_NODES + t] = g[u].y;
+        reinterpret_cast<float2*>(vtile)[t] = make_float2(g[u].x, g[u].y);
         vtile[2 * TILE_NODES + t] = g[u].z;
       }
     }
@@ -437,6 +437,10 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async8(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void load_vtile_column_async(const Params& p, float* vtile, int orgx, int x0, int x1,
@@ -445,8 +449,7 @@ __device__ __forceinline__ void load_vtile_column_async(const Params& p, float* 
     const int gi = orgx + tx;
     const float* src = reinterpret_cast<const float*>(p.gv + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4));
     const int t = (tx * TILE + ty) * TILE_Z + tz;
-    cp_async4(vtile + t, src);
-    cp_async4(vtile + TILE_NODES + t, src + 1);
+    cp_async8(vtile + 2 * t, src);
     cp_async4(vtile + 2 * TILE_NODES + t, src + 2);
   }
 }
