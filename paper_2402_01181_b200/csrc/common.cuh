@@ -92,6 +92,7 @@ struct Params {
   int nb[3];       // layout bricks per axis
   FastDiv fd_nb1, fd_nb2;  // / nb[1], / nb[2]
   int nbin[3];     // particle bins per axis
+  FastDiv fd_nbin1, fd_nbin2;  // / nbin[1], / nbin[2]
   float dx, inv_dx, dt;
   float gravity[3];
   float lo, hi[3];  // particle margin clamp (core.py:51-56), env-local
@@ -127,6 +128,14 @@ struct Params {
   const int* nwork;
   int* work_next;    // dynamic work-item counter (zeroed per launch)
 };
+
+// Bin index -> bin coordinates (x-major, z fastest) by multiply-high division.
+__device__ __forceinline__ void bin_coords(const Params& p, int bin, int& bx, int& by, int& bz) {
+  const unsigned t = p.fd_nbin2.div((unsigned)bin);
+  bz = bin - (int)t * p.nbin[2];
+  bx = (int)p.fd_nbin1.div(t);
+  by = (int)t - bx * p.nbin[1];
+}
 
 __host__ __device__ inline long long node_index(int i, int j, int k, int nby, int nbz) {
   long long b = ((long long)(i >> BRICK_SHIFT) * nby + (j >> BRICK_SHIFT)) * nbz + (k >> BRICK_SHIFT);

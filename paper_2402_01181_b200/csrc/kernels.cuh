@@ -477,9 +477,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3) g2p_stress_kernel(Params p, 
     tv.t = vtile;
     if (G2P) {
       const int bin = item.x;
-      const int bz = bin % p.nbin[2];
-      const int by = (bin / p.nbin[2]) % p.nbin[1];
-      const int bx = bin / (p.nbin[1] * p.nbin[2]);
+      int bx, by, bz;
+      bin_coords(p, bin, bx, by, bz);
       tv.org[0] = bx * BIN - MARGIN;
       tv.org[1] = by * BIN - MARGIN;
       tv.org[2] = bz * BIN - MARGIN;
@@ -669,9 +668,8 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
     int* box = boxes[par];
     const int4 item = p.work[wi];
     const int bin = item.x;
-    const int bz = bin % p.nbin[2];
-    const int by = (bin / p.nbin[2]) % p.nbin[1];
-    const int bx = bin / (p.nbin[1] * p.nbin[2]);
+    int bx, by, bz;
+    bin_coords(p, bin, bx, by, bz);
     const int org[3] = {bx * BIN - MARGIN, by * BIN - MARGIN, bz * BIN - MARGIN};
     // previous item's box (its flush ended before the last barrier)
     if (threadIdx.x < 6) boxes[par ^ 1][threadIdx.x] = threadIdx.x < 3 ? TILE : -1;
@@ -754,9 +752,8 @@ constexpr float BOUND_SAFETY = 2.0f;
 // scattered from in the previous substep, item_box).
 __device__ __forceinline__ void fused_item_geometry(const Params& p, const int4 item, int packed_box, TileVel& tv) {
   const int bin = item.x;
-  const int bz = bin % p.nbin[2];
-  const int by = (bin / p.nbin[2]) % p.nbin[1];
-  const int bx = bin / (p.nbin[1] * p.nbin[2]);
+  int bx, by, bz;
+  bin_coords(p, bin, bx, by, bz);
   tv.org[0] = bx * BIN - MARGIN;
   tv.org[1] = by * BIN - MARGIN;
   tv.org[2] = bz * BIN - MARGIN;

@@ -309,6 +309,8 @@ Params make_params(mpm_ctx* ctx) {
     if (a == 1) p.fd_nb1 = make_fastdiv(p.nb[1]);
     if (a == 2) p.fd_nb2 = make_fastdiv(p.nb[2]);
     p.nbin[a] = ctx->nbin[a];
+    if (a == 1) p.fd_nbin1 = make_fastdiv(std::max(ctx->nbin[1], 1));
+    if (a == 2) p.fd_nbin2 = make_fastdiv(std::max(ctx->nbin[2], 1));
     p.gravity[a] = (float)c.gravity[a];
     const int et = c.env_tiles[a] > 1 ? c.env_tiles[a] : 1;
     p.goff[a] = ctx->goff[a];
