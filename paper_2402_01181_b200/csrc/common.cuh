@@ -98,6 +98,7 @@ struct Params {
   float lo, hi[3];  // particle margin clamp (core.py:51-56), env-local
   int env_res[3];   // nodes per environment tile (== gres for one environment)
   float env_ext[3]; // env_res * dx
+  FastDiv fd_env[3];  // / env_res
   // slab decomposition (config 5): this context's grid is the window of the
   // global grid (gres nodes) starting at global node goff; particle positions
   // on the device are window-local (global - goff * dx)

@@ -1073,7 +1073,8 @@ __device__ __forceinline__ float4 grid_node(const Params& p, const Colliders& cs
   int li = gi, lj = gj, lk = gk;
   Colliders cs = cs_all;
   if (!single_env) {
-    const int ei = gi / p.env_res[0], ej = gj / p.env_res[1], ek = gk / p.env_res[2];
+    const int ei = (int)p.fd_env[0].div((unsigned)gi), ej = (int)p.fd_env[1].div((unsigned)gj),
+              ek = (int)p.fd_env[2].div((unsigned)gk);
     cs = env_colliders(cs_all, ei, ej, ek);
     li = gi - ei * p.env_res[0];
     lj = gj - ej * p.env_res[1];

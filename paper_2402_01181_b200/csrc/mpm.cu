@@ -318,6 +318,7 @@ Params make_params(mpm_ctx* ctx) {
     p.goffx[a] = (float)(ctx->goff[a] * c.dx);
     p.env_res[a] = p.gres[a] / et;
     p.env_ext[a] = (float)(p.env_res[a] * c.dx);
+    p.fd_env[a] = make_fastdiv(std::max(p.env_res[a], 1));
     double hd = (p.env_res[a] - 1.5 - 1.0e-7) * c.dx;
     float hf = (float)hd;
     if ((double)hf > hd) hf = std::nextafter(hf, 0.0f);
