@@ -99,6 +99,7 @@ struct Params {
   int env_res[3];   // nodes per environment tile (== gres for one environment)
   float env_ext[3]; // env_res * dx
   FastDiv fd_env[3];  // / env_res
+  float inv_env_ext[3];  // 1 / env_ext
   // slab decomposition (config 5): this context's grid is the window of the
   // global grid (gres nodes) starting at global node goff; particle positions
   // on the device are window-local (global - goff * dx)

@@ -205,9 +205,12 @@ __device__ __forceinline__ void g2p_gather(const Params& p, const float x[3], fl
 __device__ __forceinline__ void advect(const Params& p, float x[3], const float v[3]) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    // environment tile origin in window-local coordinates
-    const float org = (p.env_res[a] == p.gres[a] ? 0.0f : floorf((x[a] + p.goffx[a]) / p.env_ext[a]) * p.env_ext[a]) -
-                      p.goffx[a];
+    // environment tile origin in window-local coordinates (the walls keep a
+    // particle >= 1.5 cells inside its tile, so the reciprocal's rounding
+    // cannot move it across a tile boundary)
+    const float org =
+        (p.env_res[a] == p.gres[a] ? 0.0f : floorf((x[a] + p.goffx[a]) * p.inv_env_ext[a]) * p.env_ext[a]) -
+        p.goffx[a];
     float q = x[a] + p.dt * v[a];
     q = q < org + p.lo ? org + p.lo : q;
     q = q > org + p.hi[a] ? org + p.hi[a] : q;

@@ -319,6 +319,7 @@ Params make_params(mpm_ctx* ctx) {
     p.env_res[a] = p.gres[a] / et;
     p.env_ext[a] = (float)(p.env_res[a] * c.dx);
     p.fd_env[a] = make_fastdiv(std::max(p.env_res[a], 1));
+    p.inv_env_ext[a] = p.env_ext[a] > 0.0f ? 1.0f / p.env_ext[a] : 0.0f;
     double hd = (p.env_res[a] - 1.5 - 1.0e-7) * c.dx;
     float hf = (float)hd;
     if ((double)hf > hd) hf = std::nextafter(hf, 0.0f);
