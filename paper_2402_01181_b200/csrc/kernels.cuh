@@ -636,8 +636,11 @@ __device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int
   const int bx0 = (org[0] + x0) >> BRICK_SHIFT, by0 = (org[1] + y0) >> BRICK_SHIFT, bz0 = (org[2] + z0) >> BRICK_SHIFT;
   const int nbx = ((org[0] + x1) >> BRICK_SHIFT) - bx0 + 1, nby = ((org[1] + y1) >> BRICK_SHIFT) - by0 + 1,
             nbz = ((org[2] + z1) >> BRICK_SHIFT) - bz0 + 1;
+  // brick (bx, by, bz) of unit t by float reciprocals (exact: t < 2^10)
+  const float rbz = 1.0f / (float)nbz, rbyz = 1.0f / (float)(nby * nbz);
   for (int t = threadIdx.x; t < nbx * nby * nbz; t += blockDim.x) {
-    const int bz = t % nbz, by = (t / nbz) % nby, bx = t / (nbz * nby);
+    const int bx = (int)(((float)t + 0.5f) * rbyz), r = t - bx * nby * nbz;
+    const int by = (int)(((float)r + 0.5f) * rbz), bz = r - by * nbz;
     mark_brick(p, ((long long)((bx0 + bx) * p.nb[1] + by0 + by) * p.nb[2] + bz0 + bz) << 6);
   }
 }
