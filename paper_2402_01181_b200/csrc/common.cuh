@@ -118,6 +118,7 @@ struct Params {
   int* active_count;
   // particles
   float* P;
+  float* Pf[NF];  // per-field base pointers into P (kernel-parameter constants: one address add per access)
   int* mat;
   int* orig;
   long long cap;
@@ -183,10 +184,10 @@ __device__ __forceinline__ void stencil_rn(float xc, float inv_dx, int r, int& b
 }
 
 __device__ __forceinline__ float ldf(const Params& p, int field, long long i) {
-  return p.P[(long long)field * p.cap + i];
+  return p.Pf[field][i];
 }
 __device__ __forceinline__ void stf(const Params& p, int field, long long i, float v) {
-  p.P[(long long)field * p.cap + i] = v;
+  p.Pf[field][i] = v;
 }
 
 // F' = (I + dt C) F (kernels.py:213-231), then the Neo-Hookean affine

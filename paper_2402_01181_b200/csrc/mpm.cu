@@ -342,6 +342,7 @@ Params make_params(mpm_ctx* ctx) {
   p.active_list = ctx->active_list;
   p.active_count = ctx->counters;
   p.P = ctx->P[ctx->cur];
+  for (int f = 0; f < NF; ++f) p.Pf[f] = p.P ? p.P + (long long)f * ctx->cap : nullptr;
   p.mat = ctx->mat[ctx->cur];
   p.orig = ctx->orig[ctx->cur];
   p.cap = ctx->cap;
