@@ -42,6 +42,9 @@ constexpr int TILE = MPM_TILE;
 // plane of TILE_NODES words (z stride and plane padding tune the bank map)
 constexpr int TILE_Z = MPM_TILE_ZSTRIDE;
 constexpr int TILE_NODES = TILE * TILE * TILE_Z + MPM_PLANE_PAD;
+// the velocity tile holds (vx, vy) float2 pairs and its buffers start at
+// multiples of 3 * TILE_NODES floats: 8-byte alignment needs an even plane
+static_assert(TILE_NODES % 2 == 0, "TILE_NODES must be even (float2 velocity tile)");
 constexpr int FUSED_THREADS = 256;      // stage A (g2p_stress_kernel)
 #ifndef MPM_FUSED_THREADS
 #define MPM_FUSED_THREADS 256
@@ -181,6 +184,44 @@ __device__ __forceinline__ void stencil_rn(float xc, float inv_dx, int r, int& b
   w[1] = __fsub_rn(0.75f, __fmul_rn(t1, t1));
   w[2] = __fmul_rn(0.5f, __fmul_rn(t2, t2));
   b = bb;
+}
+
+// Packed fp32 pairs (sm_100a FFMA2 / FMUL2 / FADD2): one issue slot for two
+// lanes of fp32 math.  Measured on B200 (tools/microbench/ffma2.cu): FFMA2
+// occupies the FMA pipe for 2 cycles (no extra FLOP rate) but halves the
+// issue slots of paired math, which is what the issue-bound fused kernel
+// needs.  A scalar broadcast (f2_bc) compiles to the .F32 operand form, no MOV.
+typedef unsigned long long f2p;
+__device__ __forceinline__ f2p f2_pack(float a, float b) {
+  f2p r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2p f2_bc(float a) { return f2_pack(a, a); }
+__device__ __forceinline__ float f2_lo(f2p v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float f2_hi(f2p v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f2p f2_fma(f2p a, f2p b, f2p c) {
+  f2p d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2p f2_mul(f2p a, f2p b) {
+  f2p d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2p f2_add(f2p a, f2p b) {
+  f2p d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 
 __device__ __forceinline__ float ldf(const Params& p, int field, long long i) {

@@ -111,6 +111,11 @@ struct GlobalVel {
     const float4 g = __ldg(gv + idx);
     return make_float3(g.x, g.y, g.z);
   }
+  __device__ __forceinline__ void load2(int idx, f2p& xy, float& z) const {
+    const float4 g = __ldg(gv + idx);
+    xy = f2_pack(g.x, g.y);
+    z = g.z;
+  }
 };
 
 struct TileVel {
@@ -129,7 +134,107 @@ struct TileVel {
     const float2 xy = reinterpret_cast<const float2*>(t)[idx];
     return make_float3(xy.x, xy.y, t[2 * TILE_NODES + idx]);
   }
+  __device__ __forceinline__ void load2(int idx, f2p& xy, float& z) const {
+    xy = reinterpret_cast<const f2p*>(t)[idx];
+    z = t[2 * TILE_NODES + idx];
+  }
 };
+
+// Packed twin of g2p_gather below: the (x, y) velocity components travel as
+// one FFMA2 pair, z as scalar FFMA (186 fp issue slots per particle instead of
+// 279).  Same sums in the same order per component.
+template <class Src>
+__device__ __forceinline__ void g2p_gather_pk(const Params& p, const Src& src, const int b[3], const float f[3],
+                                              const float w[3][3], float v[3], float C[9]) {
+  int ox[3], oy[3], oz[3];
+  src.offsets(b, ox, oy, oz);
+  float wd[3][3];  // w * (offset - f)
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) wd[a][q] = w[a][q] * ((float)q - f[a]);
+  f2p v01 = 0, c001 = 0, c101 = 0, c201 = 0;
+  float vz = 0.f, c0z = 0.f, c1z = 0.f, c2z = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    f2p hv01 = 0, hj01 = 0, hk01 = 0;
+    float hvz = 0.f, hjz = 0.f, hkz = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      f2p gv01 = 0, gk01 = 0;
+      float gvz = 0.f, gkz = 0.f;
+      const int oij = ox[i] + oy[j];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        f2p g01;
+        float gz;
+        src.load2(oij + oz[k], g01, gz);
+        if (k == 0) {
+          gv01 = f2_mul(f2_bc(w[2][0]), g01);
+          gk01 = f2_mul(f2_bc(wd[2][0]), g01);
+          gvz = w[2][0] * gz;
+          gkz = wd[2][0] * gz;
+        } else {
+          gv01 = f2_fma(f2_bc(w[2][k]), g01, gv01);
+          gk01 = f2_fma(f2_bc(wd[2][k]), g01, gk01);
+          gvz = fmaf(w[2][k], gz, gvz);
+          gkz = fmaf(wd[2][k], gz, gkz);
+        }
+      }
+      if (j == 0) {
+        hv01 = f2_mul(f2_bc(w[1][0]), gv01);
+        hj01 = f2_mul(f2_bc(wd[1][0]), gv01);
+        hk01 = f2_mul(f2_bc(w[1][0]), gk01);
+        hvz = w[1][0] * gvz;
+        hjz = wd[1][0] * gvz;
+        hkz = w[1][0] * gkz;
+      } else {
+        hv01 = f2_fma(f2_bc(w[1][j]), gv01, hv01);
+        hj01 = f2_fma(f2_bc(wd[1][j]), gv01, hj01);
+        hk01 = f2_fma(f2_bc(w[1][j]), gk01, hk01);
+        hvz = fmaf(w[1][j], gvz, hvz);
+        hjz = fmaf(wd[1][j], gvz, hjz);
+        hkz = fmaf(w[1][j], gkz, hkz);
+      }
+    }
+    if (i == 0) {
+      v01 = f2_mul(f2_bc(w[0][0]), hv01);
+      c001 = f2_mul(f2_bc(wd[0][0]), hv01);
+      c101 = f2_mul(f2_bc(w[0][0]), hj01);
+      c201 = f2_mul(f2_bc(w[0][0]), hk01);
+      vz = w[0][0] * hvz;
+      c0z = wd[0][0] * hvz;
+      c1z = w[0][0] * hjz;
+      c2z = w[0][0] * hkz;
+    } else {
+      v01 = f2_fma(f2_bc(w[0][i]), hv01, v01);
+      c001 = f2_fma(f2_bc(wd[0][i]), hv01, c001);
+      c101 = f2_fma(f2_bc(w[0][i]), hj01, c101);
+      c201 = f2_fma(f2_bc(w[0][i]), hk01, c201);
+      vz = fmaf(w[0][i], hvz, vz);
+      c0z = fmaf(wd[0][i], hvz, c0z);
+      c1z = fmaf(w[0][i], hjz, c1z);
+      c2z = fmaf(w[0][i], hkz, c2z);
+    }
+  }
+  const float cc = 4.0f * p.inv_dx;  // coef * dx = 4/dx
+  const f2p cc2 = f2_bc(cc);
+  c001 = f2_mul(cc2, c001);
+  c101 = f2_mul(cc2, c101);
+  c201 = f2_mul(cc2, c201);
+  v[0] = f2_lo(v01);
+  v[1] = f2_hi(v01);
+  v[2] = vz;
+  C[0] = f2_lo(c001);
+  C[3] = f2_hi(c001);
+  C[6] = c0z * cc;
+  C[1] = f2_lo(c101);
+  C[4] = f2_hi(c101);
+  C[7] = c1z * cc;
+  C[2] = f2_lo(c201);
+  C[5] = f2_hi(c201);
+  C[8] = c2z * cc;
+}
 
 // G2P gather (kernels.py:451-516): v = sum w g, C = 4/dx^2 sum w g dp^T,
 // evaluated separably (k, then j, then i sums): 279 FMA instead of 432.
@@ -351,7 +456,7 @@ __device__ __forceinline__ float compute_payload(const Params& p, long long i, P
       if (tv) in_tile &= (b[a] - tv->org[a] >= tv->lo[a]) && (b[a] - tv->org[a] <= tv->hi[a]);
     }
     if (in_tile) {
-      g2p_gather(p, *tv, b, f, w, v, C);
+      g2p_gather_pk(p, *tv, b, f, w, v, C);
     } else {
       if (tv) FPROF_COUNT(1);
       g2p_gather(p, global_vel(p), b, f, w, v, C);
@@ -585,6 +690,97 @@ __device__ __forceinline__ void tile_scatter_rot(int* tile, const int off[4], bo
   }
 }
 
+// Rotate a 4-vector left by rot = r1 + 2 r2 (v'[s] = v[(s + rot) & 3]) in two
+// select stages: 8 FSEL instead of 12 for the 4-way select per element.
+__device__ __forceinline__ void rot4(bool r1, bool r2, float v[4]) {
+  const float a0 = r2 ? v[2] : v[0], a1 = r2 ? v[3] : v[1], a2 = r2 ? v[0] : v[2], a3 = r2 ? v[1] : v[3];
+  v[0] = r1 ? a1 : a0;
+  v[1] = r1 ? a2 : a1;
+  v[2] = r1 ? a3 : a2;
+  v[3] = r1 ? a0 : a3;
+}
+
+// Packed P2G scatter of one particle into the int32 tile (the fused kernel's
+// hot loop).  Channel c of node (i, j, k) receives
+//   w0_i w1_j w2_k (b_c + A_c . dp) S_c
+// = w2_k alpha_ij,c + (w2_k dz_k) beta_ij,c,
+//   alpha_ij = w0_i w1_j (b + A_x dx_i + A_y dy_j) S,  beta_ij = w0_i w1_j A_z S,
+// evaluated as FFMA2(w2_k, alpha, FFMA2(w2_k dz_k, beta, MAGIC)) over channel
+// pairs: 2 FFMA2 + 2 (IADD + ATOMS) per node and channel pair, instead of 6
+// scalar FFMA / FMUL + 2 (IADD + ATOMS).  Both products round onto the integer
+// grid of the magic constant (<= 1 unit of 1/S per contribution; every partial
+// term is bounded by the channel bound like the full term, so the magic range
+// holds).  Slots are rotated by the particle's rank in its cell (rot): slot s
+// carries channel (s + rot) & 3 at tile + off[s].
+__device__ __forceinline__ void tile_scatter_pk(int* tile, const int off[4], bool r1, bool r2, const float S[4],
+                                                const Payload& q, const int lc[3], float dx) {
+  // channel values scaled, then rotated into slots
+  float bs[4] = {q.mv[0] * S[0], q.mv[1] * S[1], q.mv[2] * S[2], q.m * S[3]};
+  float ax[4] = {q.A[0] * S[0], q.A[3] * S[1], q.A[6] * S[2], 0.0f};
+  float ay[4] = {q.A[1] * S[0], q.A[4] * S[1], q.A[7] * S[2], 0.0f};
+  float az[4] = {q.A[2] * S[0], q.A[5] * S[1], q.A[8] * S[2], 0.0f};
+  rot4(r1, r2, bs);
+  rot4(r1, r2, ax);
+  rot4(r1, r2, ay);
+  rot4(r1, r2, az);
+  float w[3][3], dxs[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float t0 = 1.5f - q.f[a], t1 = q.f[a] - 1.0f, t2 = q.f[a] - 0.5f;
+    w[a][0] = 0.5f * (t0 * t0);
+    w[a][1] = 0.75f - t1 * t1;
+    w[a][2] = 0.5f * (t2 * t2);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) dxs[a][o] = ((float)o - q.f[a]) * dx;
+  }
+  float wdz[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) wdz[k] = w[2][k] * dxs[2][k];
+  const f2p b01 = f2_pack(bs[0], bs[1]), b23 = f2_pack(bs[2], bs[3]);
+  const f2p ax01 = f2_pack(ax[0], ax[1]), ax23 = f2_pack(ax[2], ax[3]);
+  const f2p ay01 = f2_pack(ay[0], ay[1]), ay23 = f2_pack(ay[2], ay[3]);
+  const f2p az01 = f2_pack(az[0], az[1]), az23 = f2_pack(az[2], az[3]);
+  const f2p mm = f2_bc(MAGIC);
+#ifdef EXP_SCATTER_NOCONF  // timing experiment: conflict-free (wrong) addresses
+  int* t0 = tile + (threadIdx.x & 31) + off[0];
+#else
+  int* t0 = tile + ((lc[0] * TILE + lc[1]) * TILE_Z + lc[2]) + off[0];
+#endif
+  int* t1 = t0 - off[0] + off[1];
+  int* t2 = t0 - off[0] + off[2];
+  int* t3 = t0 - off[0] + off[3];
+#pragma unroll
+  for (int ii = 0; ii < 3; ++ii) {
+    const f2p bx01 = f2_fma(f2_bc(dxs[0][ii]), ax01, b01);
+    const f2p bx23 = f2_fma(f2_bc(dxs[0][ii]), ax23, b23);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const f2p wij = f2_bc(w[0][ii] * w[1][j]);
+      const f2p al01 = f2_mul(wij, f2_fma(f2_bc(dxs[1][j]), ay01, bx01));
+      const f2p al23 = f2_mul(wij, f2_fma(f2_bc(dxs[1][j]), ay23, bx23));
+      const f2p be01 = f2_mul(wij, az01);
+      const f2p be23 = f2_mul(wij, az23);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const f2p v01 = f2_fma(f2_bc(w[2][k]), al01, f2_fma(f2_bc(wdz[k]), be01, mm));
+        const f2p v23 = f2_fma(f2_bc(w[2][k]), al23, f2_fma(f2_bc(wdz[k]), be23, mm));
+        const int o = (ii * TILE + j) * TILE_Z + k;
+#ifdef EXP_SCATTER_STS  // timing experiment: plain stores instead of atomics
+        t0[o] = __float_as_int(f2_lo(v01)) - MAGIC_BITS;
+        t1[o] = __float_as_int(f2_hi(v01)) - MAGIC_BITS;
+        t2[o] = __float_as_int(f2_lo(v23)) - MAGIC_BITS;
+        t3[o] = __float_as_int(f2_hi(v23)) - MAGIC_BITS;
+#else
+        atomicAdd(t0 + o, __float_as_int(f2_lo(v01)) - MAGIC_BITS);
+        atomicAdd(t1 + o, __float_as_int(f2_hi(v01)) - MAGIC_BITS);
+        atomicAdd(t2 + o, __float_as_int(f2_lo(v23)) - MAGIC_BITS);
+        atomicAdd(t3 + o, __float_as_int(f2_hi(v23)) - MAGIC_BITS);
+#endif
+      }
+    }
+  }
+}
+
 // Flush an int32 fixed-point tile's node box [x0,x1]x[y0,y1]x[z0,z1] (tile
 // coordinates) into gm: one REDG.F32x4 per non-empty node, the box re-zeroed,
 // and every brick overlapping the box marked active.  The whole CTA shares the
@@ -626,7 +822,9 @@ __device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int
     }
 #pragma unroll
     for (int k = 0; k < SEG; ++k) {
+#ifndef EXP_FREEZE
       if ((a[k].x | a[k].y | a[k].z | a[k].w) == 0) continue;
+#endif
       const int gi = org[0] + xs + k;
       atomicAdd(p.gm + (gi >> BRICK_SHIFT) * xstride + yz + ((gi & 3) << 4),
                 make_float4((float)a[k].x * inv[0], (float)a[k].y * inv[1], (float)a[k].z * inv[2],
@@ -927,13 +1125,11 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
         const int crot = __popc(grp & ((1u << (threadIdx.x & 31)) - 1u)) & 3;
         const bool c1 = crot & 1, c2 = crot & 2;
         int coff[4];
-        float csc[4];
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-          coff[s2] = ((s2 + crot) & 3) * TILE_NODES;
-          csc[s2] = sel4(c1, c2, S[s2 & 3], S[(s2 + 1) & 3], S[(s2 + 2) & 3], S[(s2 + 3) & 3]);
-        }
-        tile_scatter_rot(tile, coff, c1, c2, csc, q, lc, p.dx);
+        for (int s2 = 0; s2 < 4; ++s2) coff[s2] = ((s2 + crot) & 3) * TILE_NODES;
+#ifndef EXP_NO_SCATTER
+        tile_scatter_pk(tile, coff, c1, c2, S, q, lc, p.dx);
+#endif
       }
     }
 #pragma unroll
@@ -970,7 +1166,11 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
       fused_item_geometry(p, itn, nxt_box, tn);
       fused_item_vtile_issue(p, tn, vtile);
     }
+#ifdef EXP_FREEZE  // timing experiments: the flush adds zeros (particles stay put)
+    const float inv[4] = {0.f, 0.f, 0.f, 0.f};
+#else
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
+#endif
     flush_tile<4>(p, tile, org, x0, x1, y0, y1, z0, z1, inv);
     FPROF_MARK(tf);
     if (has_next) fused_item_scales(itn, nxt_bounds, scale_s[par ^ 1]);
