@@ -245,8 +245,17 @@ int mpm_get_timing(mpm_ctx *ctx, double *out);
  * phases; pays off for small scenes, e.g. +12% at 30 K particles), "pdl"
  * (1 = fused kernel and grid op launched with programmatic dependent launch,
  * each kernel's prologue overlapping its predecessor's tail; off by default,
- * within noise at C3 and -0.4% at C4). */
+ * within noise at C3 and -0.4% at C4), "fx_shift" (test hook, 0..8: loosen
+ * the node-sum term of the fixed-point P2G scale by 2^value and divide the
+ * per-cell count limit of its overflow guard by the same factor, so the
+ * guard's float fallback is exercised on ordinary scenes; 0 in production). */
 int mpm_set_option(mpm_ctx *ctx, const char *key, int value);
+/* Cumulative device statistics of the context: index 0 = particles the
+ * fixed-point overflow guard sent down the float scatter path (their base
+ * cell already held the item's count limit, 2 x the densest cell at
+ * re-binning).  No reference counterpart (the reference scatters in fp64,
+ * kernels.py:296-313). */
+int mpm_get_stat(mpm_ctx *ctx, int index, int64_t *out);
 /* Kernel launches issued by this context so far (evidence counter; a graph
  * replay counts every kernel node it runs). */
 int64_t mpm_launch_count(mpm_ctx *ctx);

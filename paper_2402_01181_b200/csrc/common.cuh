@@ -60,6 +60,11 @@ constexpr int P2G_MIN_BLOCKS = 3;
 #define MPM_GRIDOP_MINB 2
 #endif
 constexpr int GRIDOP_MIN_BLOCKS = MPM_GRIDOP_MINB;
+// dynamic shared memory of the fused kernel: velocity tile (3 planes), int32
+// scatter tile (4 channel planes) and the per-cell particle counts of the
+// fixed-point overflow guard (1 plane); stage B: scatter tile + counts
+constexpr unsigned FUSED_SMEM = sizeof(float) * 8 * TILE_NODES;
+constexpr unsigned P2G_SMEM = sizeof(int) * 5 * TILE_NODES;
 constexpr int NPAY = 13;                // payload floats per particle: m v (3), A (9), m
 constexpr int CHUNK = 4096;               // max particles per work item (larger bins split evenly)
 constexpr int MIN_CHUNK = 256;            // small scenes: items shrink to this so every SM gets work
@@ -129,6 +134,11 @@ struct Params {
   const float* mu;
   const float* lam;
   unsigned long long* inverted;
+  // fixed-point overflow guard: stats[0] counts particles routed to the float
+  // path because their cell exceeded the item's count limit; fx_shift (test
+  // hook, default 0) scales the tile up by 2^fx_shift and the limit down
+  unsigned long long* stats;
+  int fx_shift;
   // work items (bin, start, end, 0)
   const int4* work;
   const int* nwork;

@@ -509,11 +509,22 @@ __device__ __forceinline__ void payload_bound(const Params& p, const Payload& q,
 // fits the FFMA magic-number conversion (|c S| < 2^22), and a node sum --
 // at most K * (particles per cell) * B -- stays inside int32 even if cells
 // double their occupancy before the next re-binning.
-__device__ __forceinline__ float channel_scale(float B, int maxcnt) {
+//
+// The occupancy assumption is enforced, not trusted: the scatter counts the
+// particles of every base cell in shared memory (cell_limit) and a particle
+// whose cell already holds the limit goes down the float REDG path instead,
+// so no tile node sum can leave int32 whatever the compression.  fx_shift (a
+// test hook, 0 in production) loosens the node-sum term of the scale by
+// 2^fx_shift and divides the cell limit by the same factor: without the
+// guard, dense cells would then wrap; with it the bound still holds
+// (K x limit x B x S <= 2^31) and the guard fires on ordinary scenes.
+__device__ __forceinline__ float channel_scale(float B, int maxcnt, int fx_shift = 0) {
   if (!(B > 0.f)) return 1.0f;
-  const float lim = fminf(4194304.0f / 0.4219f, 2147483648.0f / (5.36f * 2.0f * (float)max(maxcnt, 1)));
+  const float lim = fminf(4194304.0f / 0.4219f,
+                          exp2f(31.0f + (float)fx_shift) / (5.36f * 2.0f * (float)max(maxcnt, 1)));
   return exp2f(floorf(log2f(lim / B)));
 }
+__device__ __forceinline__ int cell_limit(int maxcnt, int fx_shift) { return (2 * max(maxcnt, 1)) >> fx_shift; }
 
 // One (ty, tz) column of the velocity tile, nodes tx in [x0, x1] (<= TILE):
 // loads issued in groups of 5 before their shared-memory stores.
@@ -790,7 +801,7 @@ __device__ __forceinline__ void tile_scatter_pk(int* tile, const int off[4], boo
 // (bases are clamped to [0, res-3]), so there are no bounds checks.
 template <int SEG>
 __device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int* org, int x0, int x1, int y0, int y1,
-                                           int z0, int z1, const float inv[4]) {
+                                           int z0, int z1, const float inv[4], int* ccount) {
   if (x1 < x0 + 2) return;  // empty box (every particle fell back to gm)
   const int nx = x1 - x0 + 1, ny = y1 - y0 + 1, nz = z1 - z0 + 1;
   const int nyz = ny * nz, units = nyz * ((nx + SEG - 1) / SEG);
@@ -819,6 +830,7 @@ __device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int
       tile[TILE_NODES + t] = 0;
       tile[2 * TILE_NODES + t] = 0;
       tile[3 * TILE_NODES + t] = 0;
+      ccount[t] = 0;  // the box covers every counted cell (cells [x0, x1 - 2] ...)
     }
 #pragma unroll
     for (int k = 0; k < SEG; ++k) {
@@ -856,11 +868,13 @@ __device__ __forceinline__ void flush_tile(const Params& p, int* tile, const int
 __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(Params p, const float* __restrict__ pay,
                                                                                const float4* __restrict__ bounds,
                                                                                int* __restrict__ item_box) {
-  extern __shared__ int tile[];  // SoA: 4 x TILE_NODES int32 channels (mv x, y, z, m)
+  extern __shared__ int tile[];  // SoA: 4 x TILE_NODES int32 channels (mv x, y, z, m) + per-cell counts
+  int* ccount = tile + 4 * TILE_NODES;
   __shared__ int boxes[2][6];  // double-buffered by item parity: reset one while the other is live
   __shared__ float scale_s[4];
   const int nwork = *p.nwork;
-  for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
+  unsigned guard = 0;
+  for (int t = threadIdx.x; t < 5 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
   const int rot = threadIdx.x & 3;
   const bool r1 = rot & 1, r2 = rot & 2;
@@ -880,7 +894,7 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
     if (threadIdx.x < 4) {
       const float4 bd = bounds[wi];
       const int c = threadIdx.x;
-      scale_s[c] = channel_scale(c == 0 ? bd.x : c == 1 ? bd.y : c == 2 ? bd.z : bd.w, item.w);
+      scale_s[c] = channel_scale(c == 0 ? bd.x : c == 1 ? bd.y : c == 2 ? bd.z : bd.w, item.w, p.fx_shift);
     }
     __syncthreads();
     const float S[4] = {scale_s[0], scale_s[1], scale_s[2], scale_s[3]};
@@ -912,6 +926,11 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
           lo_c[a] = min(lo_c[a], lc[a]);
           hi_c[a] = max(hi_c[a], lc[a]);
         }
+        // overflow guard: the cell's particle count against the item's limit
+        fits = atomicAdd(&ccount[(lc[0] * TILE + lc[1]) * TILE_Z + lc[2]], 1) < cell_limit(item.w, p.fx_shift);
+        guard += !fits;
+      }
+      if (fits) {
         tile_scatter_rot(tile, off, r1, r2, sc, q, lc, p.dx);
       } else {
         const float one[4] = {1.f, 1.f, 1.f, 1.f};
@@ -935,9 +954,10 @@ __global__ void __launch_bounds__(P2G_THREADS, P2G_MIN_BLOCKS) p2g_tile_kernel(P
                                  : (x0 | (y0 << 4) | (z0 << 8) | ((x1 - 2) << 12) | ((y1 - 2) << 16) | ((z1 - 2) << 20));
     }
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
-    flush_tile<2>(p, tile, org, x0, x1, y0, y1, z0, z1, inv);
+    flush_tile<2>(p, tile, org, x0, x1, y0, y1, z0, z1, inv, ccount);
     __syncthreads();
   }
+  warp_count_add(p.stats, guard);
 }
 
 // Fused steady-state substep: G2P(n) -> advect -> F update -> stress -> P2G(n+1)
@@ -985,11 +1005,11 @@ __device__ __forceinline__ void fused_item_vtile_issue(const Params& p, const Ti
 }
 
 // An item's channel scales (threads 0..3).
-__device__ __forceinline__ void fused_item_scales(const int4 item, const float4 bd, float* scale_slot) {
+__device__ __forceinline__ void fused_item_scales(const int4 item, const float4 bd, float* scale_slot, int fx_shift) {
   if (threadIdx.x < 4) {
     const int c = threadIdx.x;
     const float b = c == 0 ? bd.x * BOUND_SAFETY : c == 1 ? bd.y * BOUND_SAFETY : c == 2 ? bd.z * BOUND_SAFETY : bd.w;
-    scale_slot[c] = channel_scale(b, item.w);
+    scale_slot[c] = channel_scale(b, item.w, fx_shift);
   }
 }
 
@@ -1022,6 +1042,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
   extern __shared__ float smem[];
   float* vtile = smem;                                           // 3 x TILE_NODES
   int* tile = reinterpret_cast<int*>(smem + 3 * TILE_NODES);     // 4 x TILE_NODES
+  int* ccount = tile + 4 * TILE_NODES;                           // per-cell counts (overflow guard)
   __shared__ int boxes[2][6];
   __shared__ float scale_s[2][4];
   __shared__ int4 nxt_item;
@@ -1030,9 +1051,9 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
   __shared__ int nxt_wi;
   const int nwork = *p.nwork;
   if (zero_tile)
-    for (int t = threadIdx.x; t < 4 * TILE_NODES; t += blockDim.x) tile[t] = 0;
+    for (int t = threadIdx.x; t < 5 * TILE_NODES; t += blockDim.x) tile[t] = 0;
   if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? TILE : -1;
-  unsigned inverted = 0;
+  unsigned inverted = 0, guard = 0;
   int par = 0;
   // dynamic scheduling over the size-sorted work list: the first gridDim.x
   // items are taken in launch order, later ones from the counter
@@ -1044,7 +1065,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
     fused_item_geometry(p, it0, item_box[blockIdx.x], tv0);
     if (dep_wait) griddep_wait();
     fused_item_vtile_issue(p, tv0, vtile);
-    fused_item_scales(it0, bounds_in[blockIdx.x], scale_s[0]);
+    fused_item_scales(it0, bounds_in[blockIdx.x], scale_s[0], p.fx_shift);
     cp_async_wait_all();
   } else if (dep_wait) {
     griddep_wait();
@@ -1078,6 +1099,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
     const float S[4] = {scale_s[par][0], scale_s[par][1], scale_s[par][2], scale_s[par][3]};
     float mx[4] = {0.f, 0.f, 0.f, 0.f};
     int lo_c[3] = {TILE, TILE, TILE}, hi_c[3] = {-1, -1, -1};
+    const int climit = cell_limit(item.w, p.fx_shift);
     for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
       PRaw<true> r;
       load_raw<true>(p, i, r);
@@ -1102,6 +1124,16 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
         fits &= (lc[a] >= 0) && (lc[a] <= TILE - 3);
       }
       FPROF_COUNT(0);
+      if (fits) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lo_c[a] = min(lo_c[a], lc[a]);
+          hi_c[a] = max(hi_c[a], lc[a]);
+        }
+        // overflow guard: the cell's particle count against the item's limit
+        fits = atomicAdd(&ccount[(lc[0] * TILE + lc[1]) * TILE_Z + lc[2]], 1) < climit;
+        guard += !fits;
+      }
       if (!fits) {
         FPROF_COUNT(2);
 #ifdef FUSED_PROFILE
@@ -1110,11 +1142,6 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
         const float one[4] = {1.f, 1.f, 1.f, 1.f};
         p2g_scatter<false>(p, tile, org, q, one);
         continue;
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        lo_c[a] = min(lo_c[a], lc[a]);
-        hi_c[a] = max(hi_c[a], lc[a]);
       }
       {
         // rotate the channel order by the particle's rank among this round's
@@ -1171,9 +1198,9 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
 #else
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
 #endif
-    flush_tile<4>(p, tile, org, x0, x1, y0, y1, z0, z1, inv);
+    flush_tile<4>(p, tile, org, x0, x1, y0, y1, z0, z1, inv, ccount);
     FPROF_MARK(tf);
-    if (has_next) fused_item_scales(itn, nxt_bounds, scale_s[par ^ 1]);
+    if (has_next) fused_item_scales(itn, nxt_bounds, scale_s[par ^ 1], p.fx_shift);
     cp_async_wait_all();
     FPROF_MARK(ta0);
     __syncthreads();  // [A] flush complete (tile zero), next velocity tile ready
@@ -1192,6 +1219,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
   if (threadIdx.x == 0) atomicAdd(&g_fprof[5], 1ull);
 #endif
   warp_count_add(p.inverted, inverted);
+  warp_count_add(p.stats, guard);
 }
 
 __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,

@@ -74,6 +74,8 @@ struct mpm_ctx {
   float* lam = nullptr;
   int nmat = 0;
   unsigned long long* inverted = nullptr;
+  unsigned long long* stats = nullptr;  // [0] fixed-point guard fallbacks (cumulative)
+  int fx_shift = 0;                     // test hook: tile scale x 2^fx_shift, cell limit / 2^fx_shift
 
   // colliders
   int ncol = 0;
@@ -156,6 +158,7 @@ struct mpm_ctx {
   // CUDA graphs of whole fast-path frames, keyed by the host-side start state
   struct GraphEntry {
     int nsub, col, cur, border, dirty, timing;
+    int prows;  // pose-table rows baked into the collider tables (make_colliders clamps row to prows - 1)
     bool cclean, bclean;  // counters / bounds_out known zero at the start
     long long n;
     long long kernels;  // kernel nodes in the graph (evidence counter)
@@ -350,6 +353,8 @@ Params make_params(mpm_ctx* ctx) {
   p.mu = ctx->mu;
   p.lam = ctx->lam;
   p.inverted = ctx->inverted;
+  p.stats = ctx->stats;
+  p.fx_shift = ctx->fx_shift;
   p.work = ctx->work;
   p.nwork = ctx->counters + 1;
   p.work_next = ctx->counters + 3;
@@ -561,7 +566,7 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
     }
     {
       TimedRegion tr(ctx, 4);
-      p2g_tile_kernel<<<ctx->fused_blocks, P2G_THREADS, sizeof(int) * 4 * TILE_NODES, ctx->stream>>>(
+      p2g_tile_kernel<<<ctx->fused_blocks, P2G_THREADS, P2G_SMEM, ctx->stream>>>(
           p, ctx->pay, ctx->item_bounds, ctx->item_box);
       LAUNCHED();
     }
@@ -575,7 +580,7 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   ctx->bounds_out_clean = true;
   {
     TimedRegion tr(ctx, 5);
-    CK(launch_pdl(ctx, fused_kernel, ctx->fused_only_blocks, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES, p,
+    CK(launch_pdl(ctx, fused_kernel, ctx->fused_only_blocks, FUSED_K_THREADS, FUSED_SMEM, p,
                   ctx->item_bounds, ctx->item_bounds2, ctx->item_box));
     LAUNCHED();
   }
@@ -618,7 +623,7 @@ int launch_substeps(mpm_ctx* ctx, bool use_col, int row0, int nsub, bool last_cl
   cudaLaunchConfig_t lc_cfg = {};
   lc_cfg.gridDim = dim3(ctx->mega_blocks);
   lc_cfg.blockDim = dim3(FUSED_K_THREADS);
-  lc_cfg.dynamicSmemBytes = sizeof(float) * 7 * TILE_NODES;
+  lc_cfg.dynamicSmemBytes = FUSED_SMEM;
   lc_cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -758,15 +763,17 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
   if (!rc) rc = alloc_grid(ctx);
   if (!rc) rc = dalloc(ctx, &ctx->counters, 64);
   if (!rc) rc = dalloc(ctx, &ctx->inverted, 1);
+  if (!rc) rc = dalloc(ctx, &ctx->stats, 8);
+  if (!rc) rc = cudaMemset(ctx->stats, 0, 8 * sizeof(unsigned long long)) == cudaSuccess ? 0 : MPM_ECUDA;
   if (!rc) rc = dalloc(ctx, &ctx->flag, 1);
   if (!rc) rc = ensure_scan(ctx, ctx->nbins);
   if (!rc && cudaMemsetAsync(ctx->counters, 0, 64 * sizeof(int), ctx->stream) != cudaSuccess) rc = MPM_ECUDA;
   if (!rc) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
-    size_t smem = sizeof(int) * 4 * TILE_NODES;
+    size_t smem = P2G_SMEM;
     cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * 7 * TILE_NODES));
+                         (int)(FUSED_SMEM));
     {
       const char* e = getenv("SOFTMPM_SPLIT");
       ctx->split_mode = e && e[0] == '1';
@@ -793,10 +800,10 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
     ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
-    ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES);
+    ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_K_THREADS, FUSED_SMEM);
     cudaFuncSetAttribute(substeps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * 7 * TILE_NODES));
-    ctx->mega_blocks = persistent((const void*)substeps_kernel, FUSED_K_THREADS, sizeof(float) * 7 * TILE_NODES);
+                         (int)(FUSED_SMEM));
+    ctx->mega_blocks = persistent((const void*)substeps_kernel, FUSED_K_THREADS, FUSED_SMEM);
     {
       int coop = 0;
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->dev);
@@ -874,7 +881,7 @@ int mpm_destroy(mpm_ctx* ctx) {
                   ctx->h_send_data[0], ctx->h_send_data[1], ctx->h_recv_ids[0], ctx->h_recv_ids[1], ctx->h_recv_data[0],
                   ctx->h_recv_data[1], ctx->h_local_ids[0], ctx->h_local_ids[1],
                   ctx->mat[0], ctx->mat[1], ctx->orig[0], ctx->orig[1], ctx->key, ctx->rank, ctx->bin_count,
-                  ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->geo, ctx->pose, ctx->sdf,
+                  ctx->bin_start, ctx->bin_maxcnt, ctx->work, ctx->mu, ctx->lam, ctx->inverted, ctx->stats, ctx->geo, ctx->pose, ctx->sdf,
                   ctx->cell_count, ctx->cell_start, ctx->perm, ctx->payload, ctx->stage, ctx->flag, ctx->x0, ctx->field, ctx->mc_flag, ctx->mc_vid, ctx->mc_cnt, ctx->mc_off, ctx->mesh_v, ctx->mesh_t, ctx->enc};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1244,9 +1251,12 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
   } else {
     const int border = ctx->item_bounds == ctx->bounds_a ? 0 : 1;
     const int timing = ctx->timing ? 1 : 0;
+    // the substeps' pose pointers are baked into the graph: a table with a
+    // different row count (step() with / without pose_fn) needs its own graph
+    const int prows = col ? std::max(ctx->pose_rows, 1) : 0;
     mpm_ctx::GraphEntry* hit = nullptr;
     for (auto& g : ctx->graphs)
-      if (g.nsub == nsub && g.col == (int)col && g.cur == ctx->cur && g.border == border &&
+      if (g.nsub == nsub && g.col == (int)col && g.prows == prows && g.cur == ctx->cur && g.border == border &&
           g.dirty == ctx->grid_dirty && g.timing == timing && g.n == ctx->n && g.cclean == ctx->counters_clean &&
           g.bclean == ctx->bounds_out_clean)
         hit = &g;
@@ -1254,6 +1264,7 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       mpm_ctx::GraphEntry e{};
       e.nsub = nsub;
       e.col = (int)col;
+      e.prows = prows;
       e.cur = ctx->cur;
       e.border = border;
       e.dirty = ctx->grid_dirty;
@@ -1338,9 +1349,25 @@ int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
   } else if (!strcmp(key, "pdl")) {
     invalidate_graphs(ctx);
     ctx->pdl_on = value != 0;
+  } else if (!strcmp(key, "fx_shift")) {
+    if (value < 0 || value > 8) return fail(ctx, MPM_EINVAL, "fx_shift: 0..8");
+    invalidate_graphs(ctx);
+    ctx->fx_shift = value;
   } else {
     return fail(ctx, MPM_EINVAL, std::string("unknown option ") + key);
   }
+  return 0;
+}
+
+// Cumulative device statistics: 0 = particles the fixed-point overflow guard
+// routed to the float scatter path.
+int mpm_get_stat(mpm_ctx* ctx, int index, int64_t* out) {
+  if (!ctx || index < 0 || index >= 8 || !out) return MPM_EINVAL;
+  CK(cudaSetDevice(ctx->dev));
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, ctx->stats + index, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = (int64_t)h;
   return 0;
 }
 
@@ -2097,9 +2124,15 @@ int mpm_download_rows(mpm_ctx* ctx, int32_t* ids, double* x, double* v, double* 
 
 // Device-to-device copy (halo / migrant buffers between contexts or to
 // communication buffers).
+// The copy is complete (and ordered after all prior work of every stream of
+// the device) when the call returns: contexts run on non-blocking streams,
+// which a blocking cudaMemcpy does not order against, so the device is
+// synchronised on both sides of the copy.
 int mpm_device_copy(void* dst, const void* src, int64_t bytes) {
   if (bytes <= 0) return 0;
-  return cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDefault) == cudaSuccess ? 0 : MPM_ECUDA;
+  if (cudaDeviceSynchronize() != cudaSuccess) return MPM_ECUDA;
+  if (cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, cudaStreamPerThread) != cudaSuccess) return MPM_ECUDA;
+  return cudaStreamSynchronize(cudaStreamPerThread) == cudaSuccess ? 0 : MPM_ECUDA;
 }
 
 // Particle ids (original indices) and global positions in device order.
