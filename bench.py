@@ -62,13 +62,14 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _ncu_traffic(kernel_prefix: str):
+def _ncu_traffic(kernel_prefix: str, config: str):
     """DRAM bytes per launch of the dominant kernel from the newest committed
-    `ncu --set full` summary (profiles/rNN_ncu_<kernel>.json, written by
-    tools/ncu_summary.py from a capture of this bench), or None."""
+    `ncu --set full` summary OF THIS CONFIG (profiles/rNN_ncu_<kernel>_<config>.json,
+    written by tools/ncu_summary.py from a capture of this bench), or None --
+    a capture of another configuration is never borrowed."""
     import glob
     best = None
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_*.json"))):
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_*_{config}.json"))):
         try:
             with open(path) as f:
                 d = json.load(f)
@@ -76,7 +77,7 @@ def _ncu_traffic(kernel_prefix: str):
             continue
         for rec in d if isinstance(d, list) else [d]:
             if str(rec.get("kernel", "")).startswith(kernel_prefix) and rec.get("dram_bytes"):
-                best = (rec["dram_bytes"], os.path.relpath(path, ROOT))
+                best = (rec["dram_bytes"], os.path.relpath(path, ROOT), rec.get("dram_bytes_warm"))
     return best
 
 
@@ -425,9 +426,9 @@ def run_ours(args, rank, world, local_rank):
     assert not st.has_nan(), "simulation produced NaN"
 
     if rank != 0:
-        return
+        return None
     peak, peak_src = _peaks()
-    traffic = _ncu_traffic(dom.split(" ")[0])
+    traffic = _ncu_traffic(dom.split(" ")[0], args.config)
     avg_fused_s = fused_ms / fused_n / 1000.0
     achieved = BYTES_PER_PARTICLE_SUBSTEP * n / avg_fused_s / 1e9
     substep_s = t_dev / (args.steps * nsub)
@@ -444,6 +445,7 @@ def run_ours(args, rank, world, local_rank):
                      "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
                      "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, "
                                         f"{traffic[1]} (cold-cache ncu replay)") if traffic else None,
+                     "traffic_warm": traffic[2] if traffic else None,
                      "kernel": dom,
                      "bytes_per_launch": BYTES_PER_PARTICLE_SUBSTEP * n,
                      "mean_launch_ms": 1000.0 * avg_fused_s, "peak_source": peak_src,
@@ -479,23 +481,25 @@ def run_ours(args, rank, world, local_rank):
                                          f"restatement of kernels.py, 8 chunks, OpenMP",
                                "substep_s": times,
                                "value_1thread": rate1, "substep_s_1thread": times1}
-    print(json.dumps(out), flush=True)
+    return out
 
 
-def run_slab(args, rank, world, local_rank):
-    """Config 5 across ranks: x-slab windows, NCCL halo exchange + migration."""
+def run_slab(args, rank, world, local_rank, particles=None):
+    """Config 5 across ranks: this rank's x-slab window of the 64 M-particle
+    volume (slab.rank_window: balanced cuts), halos through peer memory (IPC
+    over NVLink; the pack kernels write into the neighbour's buffers, streams
+    ordered by device counters) or NCCL, migration once per 5-substep stretch.
+    Strong scaling: the scene is fixed, N GPUs share it.  Returns the JSON
+    object on rank 0 (None elsewhere)."""
     import torch
     import torch.distributed as tdist
-    import paper_2402_01181_b200 as sm
     from paper_2402_01181_b200 import scenes, slab
     from paper_2402_01181_b200.dist import max_over_ranks, sum_over_ranks
-    st, mats, params, _, _ = scenes.c5(count=args.particles or 64_000_000)
-    g = st.grid
-    x, v, F, C = st.x, st.v, st.F, st.C
-    wins = slab.split_state(g, x, v, F, C, st.mass, st.vol0, st.material_id, ranks=world,
-                            ghost_bricks=2, device=local_rank)
-    win = wins[rank]
-    del wins, st, x, v, F, C
+    count = particles or args.particles or 64_000_000
+    g, spawn, mats, params = scenes.c5_spawn(count=count)
+    win = slab.rank_window(g, spawn.positions, spawn.rest_volume_per_particle, mats[0].density, world, rank,
+                           ghost_bricks=2, device=local_rank)
+    del spawn
     if args.exchange == "ipc":
         ex = slab.IpcExchange(win, rank, world, device=f"cuda:{local_rank}")
     else:
@@ -516,35 +520,50 @@ def run_slab(args, rank, world, local_rank):
     el = max_over_ranks(el_local, f"cuda:{local_rank}")
     n_total = sum_over_ranks(n_local, f"cuda:{local_rank}")
     launches = sum_over_ranks(win.state._ctx.launches - launches0, f"cuda:{local_rank}")
-    if rank == 0:
-        value = n_total * params.substeps_per_frame * args.steps / el
-        peak, peak_src = _peaks()
-        achieved = BYTES_PER_PARTICLE_SUBSTEP * value / world / 1e9
-        print(json.dumps({
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"c5: {int(n_total)} particles, {g.resolution[0]}^3 grid, x-slabs over "
-                                   f"{world} GPUs ({'peer-memory (IPC/NVLink) halo' if args.exchange == 'ipc' else 'NCCL halo'}"
-                                   f" + NCCL migration; wall clock incl. exchanges)",
-                       "parallelism": f"slab x{world}",
-                       "timing": "wall clock between device-synchronised barriers around the timed frames "
-                                 "(migration syncs the host once per stretch), max over ranks"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
-                         "kernel": "whole substep per GPU incl. halo exchange and migration (no per-kernel "
-                                   "timing on the slab path)"},
-            "e2e": {"value": None, "unit": UNIT,
-                    "unavailable": "slab path keeps each window's particles on its device between frames; "
-                                   "per-rank host upload/readback is not part of this loop"},
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-        }), flush=True)
+    assert not getattr(win, "last_nan", False), "slab run produced NaN"
+    if rank != 0:
+        return None
+    value = n_total * params.substeps_per_frame * args.steps / el
+    peak, peak_src = _peaks()
+    achieved = BYTES_PER_PARTICLE_SUBSTEP * value / world / 1e9
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": f"c5: {int(n_total)} particles, {g.resolution[0]}^3 grid, x-slabs over "
+                               f"{world} GPUs ({'peer-memory (IPC/NVLink) halo' if args.exchange == 'ipc' else 'NCCL halo'}"
+                               f" + NCCL migration per 5-substep stretch, dt 1e-4), 25 substeps per step",
+                   "particles_total": int(n_total), "grid": list(g.resolution),
+                   "parallelism": f"slab x{world} (balanced x cuts)",
+                   "timing": "wall clock between device-synchronised barriers around the timed frames "
+                             "(migration syncs the host once per stretch), max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "kernel": "whole substep per GPU incl. halo exchange and migration (no per-kernel "
+                               "timing on the slab path)"},
+        "e2e": {"value": None, "unit": UNIT,
+                "unavailable": "slab path keeps each window's particles on its device between frames; "
+                               "per-rank host upload/readback is not part of this loop"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
 
 
 def _lib_count(win):
     from paper_2402_01181_b200 import _lib
     return _lib.lib().mpm_particle_count(win.state._ctx.h)
+
+
+def _respawn(args) -> int:
+    """--gpus N > 1 without a launcher: re-run this command under torchrun
+    (one rank per GPU, 127.0.0.1 rendezvous) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -557,6 +576,9 @@ def main():
     ap.add_argument("--envs", type=int, default=1024, help="c4: environments over all ranks")
     ap.add_argument("--rebin", type=int, default=None, help="override SimParams.rebin_interval")
     ap.add_argument("--particles", type=int, default=None)
+    ap.add_argument("--slab-particles", type=int, default=None,
+                    help="N > 1: particles of the C5 slab block run beside the main line "
+                         "(default 64 M; 4 M with SOFTMPM_BENCH_SHARED_GPU; 0 = skip)")
     ap.add_argument("--exchange", default="ipc", choices=["ipc", "nccl"],
                     help="c5 over ranks: halo through peer memory (pack kernels write into the neighbour's "
                          "IPC-mapped buffers) or NCCL send/recv")
@@ -564,12 +586,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3 if args.impl == "ours" else args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_respawn(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     # plumbing check only (never a measurement): SOFTMPM_BENCH_SHARED_GPU=1 lets
     # several ranks share the visible GPUs over gloo, to exercise the N > 1 path
-    # (barriers, max over ranks, sharding) on a one-GPU box
+    # (barriers, max over ranks, sharding, the slab block) on a one-GPU box
     shared = os.environ.get("SOFTMPM_BENCH_SHARED_GPU") == "1"
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -579,13 +605,28 @@ def main():
         import torch.distributed as tdist
         if shared:
             local_rank = local_rank % max(torch.cuda.device_count(), 1)
+        elif torch.cuda.device_count() < world:
+            sys.exit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPUs "
+                     "(SOFTMPM_BENCH_SHARED_GPU=1 for a plumbing run)")
         torch.cuda.set_device(local_rank)
         if shared:
             tdist.init_process_group("gloo")
         else:
             tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
-        run_ours(args, rank, world, local_rank)
+        out = run_ours(args, rank, world, local_rank)
+        if world > 1 and args.config != "c5":
+            # the north star's multi-GPU split beside the replica line: C5's
+            # 64 M-particle volume slab-decomposed over the same N GPUs
+            sp = args.slab_particles if args.slab_particles is not None else (4_000_000 if shared else 64_000_000)
+            if sp > 0:
+                blk = run_slab(args, rank, world, local_rank, particles=sp)
+                if rank == 0:
+                    if shared:
+                        blk["note"] = "ranks share one GPU (plumbing run, not a measurement)"
+                    out["slab"] = blk
+        if rank == 0 and out is not None:
+            print(json.dumps(out), flush=True)
     finally:
         if world > 1:
             import torch.distributed as tdist

@@ -149,6 +149,14 @@ int mpm_ipc_halo(mpm_ctx *ctx, int phase, int sides);
  * (SOFTMPM_IPC_EVENTS set, or no driver entry points), where the caller
  * barriers between phases 0/1 and 2/3. */
 int mpm_ipc_mode(mpm_ctx *ctx, int *device_ordered);
+/* Same-process neighbours (several windows driven by one process, on one GPU
+ * or on peer-accessible GPUs): wires window a's `side` neighbour to b (and
+ * b's opposite side to a) with direct device pointers instead of IPC
+ * handles.  mpm_ipc_halo then runs the same kernels with the streams ordered
+ * by plain events (a stream-value wait could block a later-issued signal of
+ * another stream of the process that aliases its hardware queue); the caller
+ * issues each halo phase for every window before the next phase. */
+int mpm_peer_connect(mpm_ctx *a, int side, mpm_ctx *b);
 
 /* ---- slab decomposition (BASELINE config 5) ------------------------------
  * A context can own an x-window of a larger global grid: its res[0] nodes
@@ -174,6 +182,11 @@ int mpm_halo_pack(mpm_ctx *ctx, int side, int64_t *count);
 int mpm_halo_unpack_add(mpm_ctx *ctx, int side, int64_t n);
 int mpm_halo_pack_vel(mpm_ctx *ctx, int side, int64_t *count);
 int mpm_halo_unpack_vel(mpm_ctx *ctx, int side, int64_t n);
+/* Migrants leave in two packed device row blocks (one per neighbour): field
+ * q of migrant d at rows[q * n + d], n = that side's count, 28 fields (26
+ * floats, material id, particle id) -- one contiguous copy per neighbour;
+ * *rows_cap is set to 0 (the stride is the count).  An emptied window keeps
+ * running (grid + halos) and can receive migrants. */
 int mpm_extract_migrants(mpm_ctx *ctx, int own_lo, int own_hi, int64_t *n_lo, int64_t *n_hi,
                          void **rows_lo, void **rows_hi, int64_t *rows_cap);
 int mpm_append_particles(mpm_ctx *ctx, const void *rows, int64_t m, int64_t rows_cap, int src_offset);

@@ -40,7 +40,7 @@ EXPORTS = (
     "mpm_append_particles", "mpm_reserve", "mpm_download_ids", "mpm_device_copy", "mpm_set_ids",
     "mpm_download_rows", "mpm_metrics", "mpm_splat_density", "mpm_splat_density_host",
     "mpm_marching_cubes", "mpm_mesh_fetch", "mpm_mesh_encode", "mpm_ipc_blob_size", "mpm_ipc_export", "mpm_ipc_import", "mpm_ipc_mode",
-    "mpm_ipc_halo", "mpm_get_stat",
+    "mpm_ipc_halo", "mpm_get_stat", "mpm_peer_connect",
 )
 
 
@@ -103,6 +103,7 @@ def lib():
     L.mpm_get_timing.argtypes = [_VP, _D]
     L.mpm_set_option.argtypes = [_VP, ctypes.c_char_p, ctypes.c_int]
     L.mpm_get_stat.argtypes = [_VP, ctypes.c_int, _I64]
+    L.mpm_peer_connect.argtypes = [_VP, ctypes.c_int, _VP]
     _IP = ctypes.POINTER(ctypes.c_int)
     _PP = ctypes.POINTER(_VP)
     L.mpm_set_slab.argtypes = [_VP, _IP, _IP, ctypes.c_int]

@@ -333,6 +333,10 @@ class SimState:
         n = len(self._h["x"])
         if n == 0:
             raise ParameterError("SimState has no particles")
+        if self._static_dirty and int(_lib.lib().mpm_particle_count(ctx.h)) == n and self._static_same():
+            # a read of mass / vol0 / material_id (the getter cannot know whether
+            # the caller wrote into the array) that left them unchanged
+            self._static_dirty = False
         if self._static_dirty or int(_lib.lib().mpm_particle_count(ctx.h)) != n:
             for name in list(self._dev_newer):
                 self._download((name,))
@@ -344,6 +348,7 @@ class SimState:
                      _lib.ptr(np.ascontiguousarray(self._vol0)),
                      _lib.ptr(np.ascontiguousarray(self._mat), _lib._I32))
             self._static_dirty = False
+            self._static_snap = (self._mass.copy(), self._vol0.copy(), self._mat.copy())
             self._host_dirty.clear()
             return
         if self._host_dirty:
@@ -358,6 +363,12 @@ class SimState:
             ctx.call("mpm_upload_fields", ctypes.c_uint32(mask),
                      *[_lib.ptr(arrs.get(nm)) for nm in _FIELDS])
             self._host_dirty.clear()
+
+    def _static_same(self) -> bool:
+        snap = getattr(self, "_static_snap", None)
+        return snap is not None and all(
+            a.shape == b.shape and np.array_equal(a, b)
+            for a, b in zip(snap, (self._mass, self._vol0, self._mat)))
 
     def _download(self, names) -> None:
         mask = 0

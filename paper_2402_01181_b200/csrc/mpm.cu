@@ -138,6 +138,7 @@ struct mpm_ctx {
   float4* peer_data[2] = {nullptr, nullptr};
   int* peer_cnt[2] = {nullptr, nullptr};
   float4* peer_vdata[2] = {nullptr, nullptr};
+  bool peer_local[2] = {false, false};  // peer pointers from mpm_peer_connect (same process: not IPC-mapped)
   cudaEvent_t peer_free[2] = {nullptr, nullptr}, peer_ready[2] = {nullptr, nullptr};
   // stream-memory-op protocol (no host barriers): per side, writes into the
   // neighbour's buffers done / the neighbour's writes consumed
@@ -684,7 +685,9 @@ int det_p2g(mpm_ctx* ctx) {
 }
 
 int need_particles(mpm_ctx* ctx, bool materials = true) {
-  if (ctx->n <= 0) return fail(ctx, MPM_ESTATE, "no particles uploaded");
+  // a slab window may run empty after migration (it still takes part in the
+  // halo protocol and can receive migrants): only its capacity must exist
+  if (ctx->n <= 0 && !(ctx->h_cap > 0 && ctx->cap > 0)) return fail(ctx, MPM_ESTATE, "no particles uploaded");
   if (materials && ctx->nmat <= 0) return fail(ctx, MPM_ESTATE, "no materials set");
   return 0;
 }
@@ -870,10 +873,14 @@ int mpm_destroy(mpm_ctx* ctx) {
 #endif
   invalidate_graphs(ctx);
   for (int sd = 0; sd < 2; ++sd) {
-    for (void* q : {(void*)ctx->peer_ids[sd], (void*)ctx->peer_data[sd], (void*)ctx->peer_cnt[sd], (void*)ctx->peer_vdata[sd]})
-      if (q) cudaIpcCloseMemHandle(q);
-    for (cudaEvent_t e : {ctx->ipc_free[sd], ctx->ipc_ready[sd], ctx->peer_free[sd], ctx->peer_ready[sd]})
+    if (!ctx->peer_local[sd])
+      for (void* q : {(void*)ctx->peer_ids[sd], (void*)ctx->peer_data[sd], (void*)ctx->peer_cnt[sd], (void*)ctx->peer_vdata[sd]})
+        if (q) cudaIpcCloseMemHandle(q);
+    for (cudaEvent_t e : {ctx->ipc_free[sd], ctx->ipc_ready[sd]})
       if (e) cudaEventDestroy(e);
+    if (!ctx->peer_local[sd])  // same-process peers: the neighbour owns these events
+      for (cudaEvent_t e : {ctx->peer_free[sd], ctx->peer_ready[sd]})
+        if (e) cudaEventDestroy(e);
     if (ctx->ipc_vrecv[sd]) cudaFree(ctx->ipc_vrecv[sd]);
     if (ctx->ipc_cnt[sd]) cudaFree(ctx->ipc_cnt[sd]);
   }
@@ -1737,6 +1744,53 @@ int mpm_ipc_import(mpm_ctx* ctx, int side, const void* peer) {
 
 int64_t mpm_ipc_blob_size(void) { return (int64_t)IPC_BLOB; }
 
+// Same-process neighbours (several windows driven by one process: one GPU,
+// or one GPU each with peer access): window a's `side` neighbour is b and
+// b's opposite side is a.  The peer pointers are the neighbour's own device
+// buffers, so the IPC halo kernels and the device-ordered counter protocol
+// (mpm_ipc_halo) run unchanged, without IPC handles.
+int mpm_peer_connect(mpm_ctx* a, int side, mpm_ctx* b) {
+  if (!a || !b || side < 0 || side > 1 || a == b) return MPM_EINVAL;
+  if (!a->h_cap || !b->h_cap) return fail(a, MPM_ESTATE, "peer_connect: call mpm_set_slab on both windows first");
+  mpm_ctx* w[2] = {a, b};
+  const int sd[2] = {side, 1 - side};
+  for (int k = 0; k < 2; ++k) {
+    mpm_ctx* ctx = w[k];
+    CK(cudaSetDevice(ctx->dev));
+    if (!ctx->ipc_vrecv[sd[k]]) {
+      TRY(dalloc(ctx, &ctx->ipc_vrecv[sd[k]], (size_t)(ctx->h_cap + 1) * 64));
+      TRY(dalloc(ctx, &ctx->ipc_cnt[sd[k]], 8));
+      CK(cudaMemset(ctx->ipc_cnt[sd[k]], 0, 8 * sizeof(int)));
+    }
+    if (!ctx->ipc_free[sd[k]]) {
+      CK(cudaEventCreateWithFlags(&ctx->ipc_free[sd[k]], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ipc_ready[sd[k]], cudaEventDisableTiming));
+    }
+  }
+  if (a->dev != b->dev) {
+    for (int k = 0; k < 2; ++k) {
+      mpm_ctx* ctx = w[k];
+      CK(cudaSetDevice(ctx->dev));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(w[1 - k]->dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(a, MPM_ECUDA, "peer_connect: no peer access");
+      cudaGetLastError();
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    mpm_ctx* c = w[k];
+    mpm_ctx* o = w[1 - k];
+    const int s = sd[k];
+    c->peer_ids[s] = o->h_recv_ids[1 - s];
+    c->peer_data[s] = o->h_recv_data[1 - s];
+    c->peer_cnt[s] = o->ipc_cnt[1 - s];
+    c->peer_vdata[s] = o->ipc_vrecv[1 - s];
+    c->peer_free[s] = o->ipc_free[1 - s];
+    c->peer_ready[s] = o->ipc_ready[1 - s];
+    c->peer_local[s] = true;
+  }
+  return cudaSetDevice(a->dev) == cudaSuccess ? 0 : MPM_ECUDA;
+}
+
 // Stream memory operations (driver entry points through the runtime): the
 // halo protocol orders the neighbours' streams with counters in device memory
 // -- a wait on our own counter, a write into the neighbour's (IPC-mapped,
@@ -1795,28 +1849,34 @@ int mpm_ipc_halo(mpm_ctx* ctx, int phase, int sides) {
   for (int sd = 0; sd < 2; ++sd) {
     if (!((sides >> sd) & 1)) continue;
     if (!ctx->peer_ids[sd] || !ctx->ipc_cnt[sd]) return fail(ctx, MPM_ESTATE, "ipc_halo: side not connected");
+    // same-process neighbours order their streams with plain events: a
+    // stream wait on a value that a LATER-issued operation of another stream
+    // of this process writes can deadlock when both streams alias one
+    // hardware work queue; an event wait always follows its record in host
+    // order (the caller issues each phase for every window before the next)
+    const bool ordered_sd = ordered && !ctx->peer_local[sd];
     // [0] records received, [1] received last, [2] records sent,
     // [4] neighbour's writes ready (set by it), [5] our writes consumed (set by it)
     int* cnt = ctx->ipc_cnt[sd];
     int* pcnt = ctx->peer_cnt[sd];
     // before writing into the neighbour: it consumed our previous write
     auto before_write = [&]() -> int {
-      if (ordered) return ipc_wait(ctx, cnt, 5, ctx->ipc_writes[sd]);
+      if (ordered_sd) return ipc_wait(ctx, cnt, 5, ctx->ipc_writes[sd]);
       CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_free[sd], 0));
       return 0;
     };
     auto after_write = [&]() -> int {
-      if (ordered) return ipc_signal(ctx, pcnt, 4, ++ctx->ipc_writes[sd]);
+      if (ordered_sd) return ipc_signal(ctx, pcnt, 4, ++ctx->ipc_writes[sd]);
       CK(cudaEventRecord(ctx->ipc_ready[sd], ctx->stream));
       return 0;
     };
     auto before_read = [&]() -> int {
-      if (ordered) return ipc_wait(ctx, cnt, 4, ++ctx->ipc_reads[sd]);
+      if (ordered_sd) return ipc_wait(ctx, cnt, 4, ++ctx->ipc_reads[sd]);
       CK(cudaStreamWaitEvent(ctx->stream, ctx->peer_ready[sd], 0));
       return 0;
     };
     auto after_read = [&]() -> int {
-      if (ordered) return ipc_signal(ctx, pcnt, 5, ctx->ipc_reads[sd]);
+      if (ordered_sd) return ipc_signal(ctx, pcnt, 5, ctx->ipc_reads[sd]);
       CK(cudaEventRecord(ctx->ipc_free[sd], ctx->stream));
       return 0;
     };
@@ -2001,7 +2061,7 @@ int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, in
   const int nxt = ctx->cur ^ 1;
   migrant_scatter_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
       p, flag, posv[0], posv[1], posv[2], ctx->P[nxt], ctx->mat[nxt], ctx->orig[nxt], ctx->mig_rows[0], ctx->mig_rows[1],
-      ctx->mig_cap);
+      (long long)totals[1], (long long)totals[2]);
   LAUNCHED();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->cur = nxt;
@@ -2010,7 +2070,7 @@ int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, in
   if (n_hi) *n_hi = totals[2];
   if (rows_lo) *rows_lo = ctx->mig_rows[0];
   if (rows_hi) *rows_hi = ctx->mig_rows[1];
-  if (rows_cap) *rows_cap = ctx->mig_cap;
+  if (rows_cap) *rows_cap = 0;  // packed: each side's rows are a contiguous ROWS x count block
   return 0;
 }
 

@@ -166,9 +166,11 @@ __global__ void migrant_flag_kernel(Params p, int own_lo, int own_hi, int* flag)
 }
 
 // Stable compaction by flag class via exclusive scans: dst row = pos[class][i].
+// Migrant rows are packed per side: field q of row d at out[q * m + d], m =
+// that side's migrant count (one contiguous ROWS x m block per neighbour).
 __global__ void migrant_scatter_kernel(Params p, const int* flag, const int* pos_keep, const int* pos_lo,
                                        const int* pos_hi, float* keep_P, int* keep_mat, int* keep_orig,
-                                       float* out_lo, float* out_hi, long long out_cap) {
+                                       float* out_lo, float* out_hi, long long m_lo, long long m_hi) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   const int f = flag[i];
@@ -182,6 +184,7 @@ __global__ void migrant_scatter_kernel(Params p, const int* flag, const int* pos
     // row layout: NF floats, mat, orig (as float bits)
     float* out = f == 1 ? out_lo : out_hi;
     const long long d = f == 1 ? pos_lo[i] : pos_hi[i];
+    const long long out_cap = f == 1 ? m_lo : m_hi;
 #pragma unroll
     for (int q = 0; q < NF; ++q) out[q * out_cap + d] = ldf(p, q, i);
     out[NF * out_cap + d] = __int_as_float(p.mat[i]);

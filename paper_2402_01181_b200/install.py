@@ -39,14 +39,42 @@ def _shadow(ref_state):
     return sh
 
 
-def _writeback(ref_state, sh, fields=("x", "v", "F", "C"), grid=True):
+def _writeback(ref_state, sh, fields=("x", "v", "F", "C"), grid=True, collision=False):
     for nm in fields:
         np.copyto(getattr(ref_state, nm), getattr(sh, nm))
+    d = ref_state.__dict__
     if grid:
-        np.copyto(ref_state.grid_mv, sh.grid_mv)
-        np.copyto(ref_state.grid_m, sh.grid_m)
+        # the dense grid (537 MB at 256^3) is copied back only when read
+        d.setdefault("_b200_stale", set()).update(("grid_mv", "grid_m"))
+    if collision:
+        d.setdefault("_b200_stale", set()).add("_collision")
     ref_state.time = sh.time
     ref_state.step_count = sh.step_count
+
+
+def _lazy_attr(name):
+    """Class-level data descriptor over a reference SimState dataclass field:
+    values written by the device path are fetched from the shadow state on
+    first read (grid_mv / grid_m downloaded into the caller's own arrays,
+    _collision = the merged field of the last substep, core.py:307-309)."""
+    def get(self):
+        d = self.__dict__
+        stale = d.get("_b200_stale")
+        if stale and name in stale:
+            stale.discard(name)
+            sh = d.get("_b200_shadow")
+            if name == "_collision":
+                d[name] = sh._collision
+            else:
+                np.copyto(d[name], getattr(sh, name))
+        return d.get(name)
+
+    def set(self, value):
+        d = self.__dict__
+        if d.get("_b200_stale"):
+            d["_b200_stale"].discard(name)
+        d[name] = value
+    return property(get, set)
 
 
 def _params(p):
@@ -68,6 +96,10 @@ def install(softmpm_module):
         return softmpm_module
     for name in ("p2g", "grid_update", "g2p_advect", "substep", "step"):
         _SAVED[name] = (getattr(core, name), getattr(softmpm_module, name, None))
+    cls = core.SimState
+    _SAVED["__lazy__"] = (cls, {a: cls.__dict__.get(a) for a in ("grid_mv", "grid_m", "_collision")})
+    for a in ("grid_mv", "grid_m", "_collision"):
+        setattr(cls, a, _lazy_attr(a))
 
     def p2g(state, materials, params):
         sh = _shadow(state)
@@ -91,14 +123,14 @@ def install(softmpm_module):
     def substep(state, materials, params, colliders=None):
         sh = _shadow(state)
         inv = _core.substep(sh, _mats(materials), _params(params), _colliders(state, colliders))
-        _writeback(state, sh)
+        _writeback(state, sh, collision=bool(colliders))
         return inv
 
     def step(state, materials, params, colliders=None, pose_fn=None):
         sh = _shadow(state)
         rep = _core.step(sh, _mats(materials), _params(params), _colliders(state, colliders),
                          pose_fn)
-        _writeback(state, sh)
+        _writeback(state, sh, collision=bool(colliders))
         return softmpm_module.core.StepReport(rep.step_index, rep.sim_time, rep.timings_ms,
                                               rep.inverted_particles)
 
@@ -118,6 +150,12 @@ def _colliders(state, colliders):
 
 def uninstall(softmpm_module):
     core = softmpm_module.core
+    cls, attrs = _SAVED.pop("__lazy__", (None, {}))
+    for a, orig in attrs.items():
+        if orig is None:
+            delattr(cls, a)
+        else:
+            setattr(cls, a, orig)
     for name, (orig_core, orig_top) in _SAVED.items():
         setattr(core, name, orig_core)
         if orig_top is not None:

@@ -109,17 +109,23 @@ def c4_envs(n_envs: int = 1024, count: int = 30_000, res: int = 64, first_seed: 
     return EnvBatch(states, cols), mats, SimParams(), fns
 
 
+def c5_spawn(count: int = 64_000_000, res: int = 1024, seed: int = 1):
+    """Config 5's grid, particle spawn, materials and params without the
+    SimState (slab ranks build only their own window: slab.rank_window)."""
+    grid = Grid((res, res, res))
+    spawn = sample_box((0.5, 0.065, 0.5), (0.4, 0.1, 0.4), count, seed=seed, grid=grid)
+    return grid, spawn, _material(), SimParams(dt=1.0e-4, rebin_interval=5)
+
+
 def c5(count: int = 64_000_000, res: int = 1024, seed: int = 1):
     """Config 5: a large tissue volume (0.4 x 0.1 x 0.4 m, ~3.7 particles per
     cell at 1024^3) settling on the floor under gravity; slab-decomposed along x
     across ranks by slab.split_state / bench.py --config c5.  dt = 1e-4: at
     dx ~ 1 mm the default 5e-4 breaks the explicit CFL bound (elastic wave
     speed ~3.7 m/s -> c dt / dx ~ 1.9), for the reference scheme as well."""
-    grid = Grid((res, res, res))
-    mats = _material()
-    spawn = sample_box((0.5, 0.065, 0.5), (0.4, 0.1, 0.4), count, seed=seed, grid=grid)
+    grid, spawn, mats, params = c5_spawn(count, res, seed)
     st = SimState.from_spawns(grid, [spawn], mats)
-    return st, mats, SimParams(dt=1.0e-4, rebin_interval=5), [], None
+    return st, mats, params, [], None
 
 
 BUILDERS = {"c1": c1, "c2": c2, "c3": c3, "c5": c5}

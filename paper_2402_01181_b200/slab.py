@@ -36,6 +36,38 @@ NF = 26          # particle float fields (csrc/common.cuh)
 ROWS = NF + 2    # + material id + particle id
 
 
+def balanced_partition(base_x, res_x: int, ranks: int) -> list[tuple[int, int]]:
+    """Owned base-cell x ranges [lo, hi) (multiples of 4 nodes) holding about
+    the same number of particles each: cuts at the particle-count quantiles of
+    the 4-node brick columns, every window at least one column wide.  Raises
+    ParameterError when fewer brick columns hold particles than there are
+    ranks (some window would start empty)."""
+    bricks = res_x // 4
+    if ranks < 1 or bricks < ranks:
+        raise ParameterError("too many slabs for the grid")
+    col = np.clip(np.asarray(base_x, dtype=np.int64) // 4, 0, bricks - 1)
+    hist = np.bincount(col, minlength=bricks).astype(np.float64)
+    if np.count_nonzero(hist) < ranks:
+        raise ParameterError(f"only {np.count_nonzero(hist)} occupied 4-node x columns for {ranks} slabs")
+    cum = np.cumsum(hist)
+    total = cum[-1]
+    cuts, lo = [], 0
+    for r in range(1, ranks):
+        # first column boundary whose cumulative count reaches r/ranks of the total,
+        # leaving at least one column and one occupied column for every later rank
+        c = int(np.searchsorted(cum, total * r / ranks, side="left")) + 1
+        c = max(c, lo + 1)
+        while c < bricks and cum[c - 1] - (cum[lo - 1] if lo else 0.0) == 0:
+            c += 1  # this window must hold particles
+        c = min(c, bricks - (ranks - r))
+        while np.count_nonzero(hist[c:]) < ranks - r:
+            c -= 1
+        cuts.append(c)
+        lo = c
+    edges = [0] + cuts + [bricks]
+    return [(4 * a, 4 * b) for a, b in zip(edges, edges[1:])]
+
+
 def partition(res_x: int, ranks: int, weights=None) -> list[tuple[int, int]]:
     """Owned base-cell x ranges [lo, hi) per rank, multiples of 4 nodes."""
     bricks = res_x // 4
@@ -143,15 +175,15 @@ class LocalExchange:
         return recv
 
     def migrate(self, outgoing):
-        """outgoing[r] = {side: (ptr, m, cap)} -> appended to the neighbours."""
-        L = _lib.lib()
+        """outgoing[r] = {side: (ptr, m)} (packed ROWS x m blocks) -> appended
+        to the neighbours."""
         for r, out in enumerate(outgoing):
-            for side, (ptr, m, cap) in out.items():
+            for side, (ptr, m) in out.items():
                 nb = r - 1 if side == 0 else r + 1
                 if m == 0 or nb < 0 or nb >= len(self.w):
                     continue
                 self.w[nb].state._ctx.call("mpm_append_particles", ptr, ctypes.c_int64(m),
-                                           ctypes.c_int64(cap), self.w[r].offset)
+                                           ctypes.c_int64(m), self.w[r].offset)
 
 
 class TorchExchange:
@@ -299,7 +331,79 @@ def step_local(windows, exchange: LocalExchange, materials, params, colliders=No
                                        ctypes.c_int64())
             win.state._ctx.call("mpm_extract_migrants", win.own[0], win.own[1], ctypes.byref(nlo),
                                 ctypes.byref(nhi), ctypes.byref(plo), ctypes.byref(phi), ctypes.byref(cap))
-            outgoing.append({0: (plo.value, nlo.value, cap.value), 1: (phi.value, nhi.value, cap.value)})
+            outgoing.append({0: (plo.value, nlo.value), 1: (phi.value, nhi.value)})
+        exchange.migrate(outgoing)
+        s += span
+    return inverted
+
+
+class PeerExchange(LocalExchange):
+    """All windows in this process, exchanged through peer memory: the halo
+    pack kernels write straight into the neighbour window's receive buffers
+    (mpm_peer_connect + mpm_ipc_halo, the same kernels as IpcExchange between
+    processes) and the windows' streams are ordered by events recorded and
+    waited in host issue order, so a substep issues no host synchronisation
+    at all."""
+
+    def __init__(self, windows):
+        super().__init__(windows)
+        self.sides = []
+        self.connected = False
+
+    def connect(self):
+        if self.connected:
+            return
+        L = _lib.lib()
+        n = len(self.w)
+        for r in range(n - 1):
+            h = self.w[r].state._ctx.h
+            _lib.check(L.mpm_peer_connect(h, 1, self.w[r + 1].state._ctx.h), h, "mpm_peer_connect")
+        self.sides = [(1 if r > 0 else 0) | (2 if r < n - 1 else 0) for r in range(n)]
+        self.connected = True
+
+
+def step_local_peer(windows, exchange: PeerExchange, materials, params, colliders=None, pose_rows=None):
+    """One frame of every window in this process with peer-memory halos:
+    per substep every window's particle stage, halo phases and grid op are
+    enqueued on its own stream without host synchronisation; the host syncs
+    once per re-binning stretch (inverted count + migration).  Returns the
+    frame's inverted-element count summed over windows."""
+    nsub = params.substeps_per_frame
+    L = int(params.rebin_interval)
+    inverted = 0
+    for win in windows:
+        win.configure(materials, params, colliders, pose_rows)
+    exchange.connect()
+    ctxs = [win.state._ctx for win in windows]
+    sides = exchange.sides
+    s = 0
+    while s < nsub:
+        span = min(L, nsub - s)
+        for c in ctxs:
+            c.call("mpm_stage_begin", nsub, int(bool(colliders)))
+        for t in range(span):
+            sub = s + t
+            for c in ctxs:
+                c.call("mpm_stage_particles", int(t == 0))
+            # each halo phase is issued for every window before the next phase
+            # (the event waits of a phase follow the neighbours' records)
+            for phase in (0, 1, None, 2, 3):
+                for r, c in enumerate(ctxs):
+                    if phase is None:
+                        c.call("mpm_stage_grid", sub, int(sub != nsub - 1))
+                    elif sides[r]:
+                        c.call("mpm_ipc_halo", phase, sides[r])
+        for c in ctxs:
+            inv = ctypes.c_int64()
+            c.call("mpm_stage_end", ctypes.byref(inv))
+            inverted += inv.value
+        outgoing = []
+        for win in windows:
+            nlo, nhi, plo, phi, cap = (ctypes.c_int64(), ctypes.c_int64(), _lib._VP(), _lib._VP(),
+                                       ctypes.c_int64())
+            win.state._ctx.call("mpm_extract_migrants", win.own[0], win.own[1], ctypes.byref(nlo),
+                                ctypes.byref(nhi), ctypes.byref(plo), ctypes.byref(phi), ctypes.byref(cap))
+            outgoing.append({0: (plo.value, nlo.value), 1: (phi.value, nhi.value)})
         exchange.migrate(outgoing)
         s += span
     return inverted
@@ -320,7 +424,9 @@ def split_state(grid: core.Grid, x, v, F, C, mass, vol0, mat, ranks: int, ghost_
     """Cut a global particle set into slab windows (base-cell ownership)."""
     dx = grid.dx
     base = np.floor(np.asarray(x)[:, 0] / dx - 0.5).astype(np.int64)
-    parts = partition(grid.resolution[0], ranks)
+    # windows of equal particle count (a scene that does not span the domain
+    # would otherwise leave the outer windows empty)
+    parts = balanced_partition(base, grid.resolution[0], ranks)
     wins = []
     ids = np.arange(len(x), dtype=np.int32)
     for own in parts:
@@ -329,6 +435,24 @@ def split_state(grid: core.Grid, x, v, F, C, mass, vol0, mat, ranks: int, ghost_
         wins.append(SlabWindow(grid, own, x[sel], v[sel], F[sel], C[sel], mass[sel], vol0[sel], mat[sel],
                                ids[sel], ghost_bricks=ghost_bricks, device=device, capacity=cap))
     return wins
+
+
+def rank_window(grid: core.Grid, positions, rest_volume: float, density: float, ranks: int, rank: int,
+                ghost_bricks: int = 2, device: int | None = None, capacity_factor: float = 1.5) -> SlabWindow:
+    """This rank's window of a fresh scene (F = I, v = C = 0, one material),
+    built from the global positions without materialising the global
+    v / F / C arrays (a 64 M-particle scene on every rank of a node would
+    otherwise hold 14 GB of host state per rank).  Same cuts as split_state."""
+    x = np.asarray(positions)
+    base = np.floor(x[:, 0] / grid.dx - 0.5).astype(np.int64)
+    own = balanced_partition(base, grid.resolution[0], ranks)[rank]
+    sel = np.nonzero((base >= own[0]) & (base < own[1]))[0]
+    n = len(sel)
+    cap = int(max(16, capacity_factor * n + 1024))
+    vol = np.full(n, rest_volume)
+    return SlabWindow(grid, own, x[sel], np.zeros((n, 3)), np.broadcast_to(np.eye(3), (n, 3, 3)),
+                      np.zeros((n, 3, 3)), density * vol, vol, np.zeros(n, np.int32), sel.astype(np.int32),
+                      ghost_bricks=ghost_bricks, device=device, capacity=cap)
 
 
 # ---------------------------------------------------------------------------
@@ -432,8 +556,7 @@ def step_distributed(win: SlabWindow, ex, materials, params, colliders=None, pos
         for side, nb in nbs.items():
             ptr, m = mine[side]
             t = _dev_tensor((ROWS, m), torch.float32, ex.device)
-            for f in range(ROWS):
-                L.mpm_device_copy(t.data_ptr() + 4 * f * m, ptr + 4 * f * cap.value, 4 * m)
+            L.mpm_device_copy(t.data_ptr(), ptr, 4 * ROWS * m)  # packed ROWS x m block: one copy
             send[nb] = t
         ops_out = ex._sendrecv({nb: t.reshape(-1) for nb, t in send.items()},
                                {nb: (ROWS * got[nb],) for nb in got}, torch.float32)
@@ -446,4 +569,13 @@ def step_distributed(win: SlabWindow, ex, materials, params, colliders=None, pos
                          offsets[nb])
         torch.cuda.synchronize()
         s += span
-    return inverted
+    # the frame's inverted-element count and NaN flag over all windows (the
+    # reference's StepReport.inverted_particles is global, core.py:316-320):
+    # one all-reduce per frame
+    import torch.distributed as dist
+    flag = ctypes.c_int(0)
+    ctx.call("mpm_has_nan", ctypes.byref(flag))
+    red = torch.tensor([inverted, int(flag.value != 0)], dtype=torch.int64, device=ex.device)
+    dist.all_reduce(red)
+    win.last_nan = bool(red[1].item())
+    return int(red[0].item())

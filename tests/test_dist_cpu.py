@@ -103,3 +103,27 @@ def test_slab_partition():
         assert all(lo % 4 == 0 and hi % 4 == 0 for lo, hi in parts)
         widths = [hi - lo for lo, hi in parts]
         assert max(widths) - min(widths) <= 4
+
+
+def test_balanced_partition_narrow_scene():
+    """a scene spanning x in [0.3, 0.7] cut for 4 and 8 ranks --
+    every window holds particles, counts within a brick column of equal."""
+    import numpy as np
+    from paper_2402_01181_b200.slab import balanced_partition
+    rng = np.random.default_rng(0)
+    res = 1024
+    base = np.floor(rng.uniform(0.3, 0.7, 2_000_000) * res - 0.5).astype(np.int64)
+    for ranks in (2, 4, 8):
+        parts = balanced_partition(base, res, ranks)
+        assert parts[0][0] == 0 and parts[-1][1] == res
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        assert all(lo % 4 == 0 and hi % 4 == 0 and hi > lo for lo, hi in parts)
+        counts = [int(((base >= lo) & (base < hi)).sum()) for lo, hi in parts]
+        assert min(counts) > 0
+        per_col = len(base) / (0.4 * res / 4)
+        assert max(counts) - min(counts) <= 2 * per_col, counts
+    # a scene occupying fewer columns than ranks cannot be cut
+    import pytest
+    from paper_2402_01181_b200.errors import ParameterError
+    with pytest.raises(ParameterError):
+        balanced_partition(np.full(100, 40), 64, 4)
