@@ -185,6 +185,63 @@ def cpu_oracle_rate(config, particles, seed, substeps, threads):
     return n / dt_med, times[1:], n
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference():
+    """The unmodified reference package (softmpm, numba) installed by
+    tools/install_reference.sh into baseline/_ref, or None.  Its off-path
+    scikit-image import is stubbed; numba's cache goes to /tmp."""
+    if not os.path.isdir(os.path.join(REF_DIR, "softmpm")):
+        return None
+    import types
+    if "skimage" not in sys.modules:
+        sk = types.ModuleType("skimage")
+        sk.measure = types.ModuleType("skimage.measure")
+        sys.modules["skimage"], sys.modules["skimage.measure"] = sk, sk.measure
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/softmpm_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import softmpm
+        return softmpm
+    except Exception:
+        return None
+
+
+def numba_reference_rate(config, particles, seed, substeps, threads, warmup=1):
+    """The reference's own CPU path -- softmpm.core.substep (numba kernels,
+    kernels.py:161-534) with the per-substep pose_fn, as core.step runs it --
+    on the same scene (positions, tool path), numba threads = `threads`.
+    Returns (particle-substeps/s, per-substep seconds, n) or None."""
+    ref = _import_reference()
+    if ref is None:
+        return None
+    import numba
+    numba.set_num_threads(max(1, min(threads, numba.config.NUMBA_NUM_THREADS)))
+    st, mats, params, cols, pose_fn = build_scene(config, particles, seed)
+    g = st.grid
+    rst = ref.SimState(grid=ref.Grid(resolution=g.resolution, extent=g.extent), x=st.x.copy(), v=st.v.copy(),
+                       F=st.F.copy(), C=st.C.copy(), mass=st.mass.copy(), vol0=st.vol0.copy(),
+                       material_id=st.material_id.copy())
+    rmats = [ref.Material(m.young_modulus, m.poisson_ratio, m.density) for m in mats]
+    rparams = ref.SimParams(dt=params.dt)
+    rcols = [ref.RigidCollider(id=c.id, shape=ref.Box(np.asarray(c.shape.half_extents)),
+                               friction_mu=c.friction_mu) for c in cols]
+    t = 0.0
+    times = []
+    for i in range(warmup + substeps):
+        t0 = time.perf_counter()
+        if rcols:
+            pose_fn(rcols, t)
+        ref.core.substep(rst, rmats, rparams, rcols)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+        t += params.dt
+    n = st.particle_count
+    return n / float(np.median(times)), times, n
+
+
 def scene_workload(config, n, res, ncols):
     return (f"{config}: {n} particles/GPU, {res}^3 grid, {ncols} tool(s)"
             + (" pressing 3 cm at 0.5 m/s then holding" if config == "c3" else "")
@@ -195,8 +252,10 @@ def scene_workload(config, n, res, ncols):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from oracle import oracle as O
     threads = os.cpu_count() or 1
+    if args.config in ("c1", "c3") and _import_reference() is not None:
+        return run_reference_numba(args, world, threads)
+    from oracle import oracle as O
     O.set_threads(threads)
     import paper_2402_01181_b200 as sm
     st, mats, params, cols, pose_fn = build_scene(args.config, args.particles, 1)
@@ -230,6 +289,33 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"each step = 1 substep of the full {args.config} scene "
                                    f"(O1 fp64 C restatement of kernels.py, 8 chunks, OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_reference_numba(args, world, threads):
+    """Reference arm on the reference's own code: softmpm.core.substep (numba,
+    all host threads) from baseline/_ref, one substep of the full scene per
+    timed step (JIT compile inside the warm-up steps)."""
+    rate, times, n = numba_reference_rate(args.config, args.particles, 1, args.steps, threads,
+                                          warmup=max(1, args.warmup))
+    st, _, params, cols, _ = build_scene(args.config, args.particles, 1)
+    g = st.grid
+    tot = float(sum(times))
+    value = n * len(times) / tot
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": scene_workload(args.config, n, g.resolution[0], len(cols)),
+                   "particles_per_gpu": n, "grid": list(g.resolution),
+                   "substeps_per_step": params.substeps_per_frame,
+                   "parallelism": f"CPU, {threads} numba threads (each timed step is one substep of the frame)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"each step = 1 substep of the full {args.config} scene: the unmodified "
+                                   f"reference softmpm.core.substep (numba, baseline/_ref) with its pose_fn"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -481,6 +567,18 @@ def run_ours(args, rank, world, local_rank):
                                          f"restatement of kernels.py, 8 chunks, OpenMP",
                                "substep_s": times,
                                "value_1thread": rate1, "substep_s_1thread": times1}
+        if args.config in ("c1", "c3"):  # box tools / none (the C2 SDF jaws stay on the port)
+            try:
+                r = numba_reference_rate(args.config, args.particles, 1, args.cpu_substeps, threads)
+            except Exception as e:  # the port above stays the baseline
+                r = None
+                out["cpu_baseline"]["reference_numba_error"] = str(e)[:200]
+            if r is not None:
+                out["cpu_baseline"]["reference_numba"] = {
+                    "value": r[0], "unit": UNIT, "cores": threads, "kind": "reference",
+                    "substep_s": r[1],
+                    "sample": f"{args.cpu_substeps} substeps (after 1 warm-up incl. JIT) of the same scene through "
+                              f"the unmodified reference softmpm.core.substep (numba, baseline/_ref)"}
     return out
 
 

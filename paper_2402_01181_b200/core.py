@@ -374,9 +374,16 @@ class SimState:
         mask = 0
         for nm in names:
             mask |= _FIELD_BIT[nm]
+        fresh = {nm: np.empty_like(self._h[nm]) for nm in names}
         self._ctx.call("mpm_download_particles", ctypes.c_uint32(mask),
-                       *[_lib.ptr(self._h[nm] if nm in names else None) for nm in _FIELDS])
+                       *[_lib.ptr(fresh.get(nm)) for nm in _FIELDS])
         for nm in names:
+            # the device holds fp32: where its value is the fp32 rounding of
+            # the host's last value (the kernels left it unchanged), keep the
+            # host's fp64 value instead of the rounded one (e.g. G2P with a
+            # zero velocity field leaves x bit-identical, test_transfers.py:121)
+            old, new = self._h[nm], fresh[nm]
+            np.copyto(old, new, where=new != old.astype(np.float32))  # in place: callers may hold the array
             self._dev_newer.discard(nm)
 
     def _download_grid(self) -> None:

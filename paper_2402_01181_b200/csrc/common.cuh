@@ -63,7 +63,10 @@ constexpr int GRIDOP_MIN_BLOCKS = MPM_GRIDOP_MINB;
 // dynamic shared memory of the fused kernel: velocity tile (3 planes), int32
 // scatter tile (4 channel planes) and the per-cell particle counts of the
 // fixed-point overflow guard (1 plane); stage B: scatter tile + counts
-constexpr unsigned FUSED_SMEM = sizeof(float) * 8 * TILE_NODES;
+#ifndef EXP_SMEM_PAD
+#define EXP_SMEM_PAD 0  // timing experiment: extra shared memory per fused CTA (occupancy sensitivity)
+#endif
+constexpr unsigned FUSED_SMEM = sizeof(float) * 8 * TILE_NODES + EXP_SMEM_PAD;
 constexpr unsigned P2G_SMEM = sizeof(int) * 5 * TILE_NODES;
 constexpr int NPAY = 13;                // payload floats per particle: m v (3), A (9), m
 constexpr int CHUNK = 4096;               // max particles per work item (larger bins split evenly)
@@ -209,13 +212,13 @@ __device__ __forceinline__ f2p f2_pack(float a, float b) {
 }
 __device__ __forceinline__ f2p f2_bc(float a) { return f2_pack(a, a); }
 __device__ __forceinline__ float f2_lo(f2p v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  float a;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(a) : "l"(v));
   return a;
 }
 __device__ __forceinline__ float f2_hi(f2p v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  float b;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(b) : "l"(v));
   return b;
 }
 __device__ __forceinline__ f2p f2_fma(f2p a, f2p b, f2p c) {

@@ -77,11 +77,15 @@ def _lazy_attr(name):
     return property(get, set)
 
 
+_MODE = {"deterministic": False}
+
+
 def _params(p):
     return _core.SimParams(dt=p.dt, substeps_per_frame=p.substeps_per_frame, gravity=tuple(p.gravity),
                            boundary_width=p.boundary_width, boundary=p.boundary,
                            collision_theta=p.collision_theta,
-                           accumulation_chunks=p.accumulation_chunks)
+                           accumulation_chunks=p.accumulation_chunks,
+                           deterministic=_MODE["deterministic"])
 
 
 def _mats(materials):
@@ -89,9 +93,14 @@ def _mats(materials):
     return [Material(m.young_modulus, m.poisson_ratio, m.density) for m in materials]
 
 
-def install(softmpm_module):
-    """Patch the reference package in place; returns the module."""
+def install(softmpm_module, deterministic: bool = False):
+    """Patch the reference package in place; returns the module.
+
+    deterministic=True runs every substep in the sorted-order deterministic
+    mode (bitwise reproducible, like the reference's fixed-chunk accumulation,
+    kernels.py:8-12) instead of the fast atomic mode."""
     core = softmpm_module.core
+    _MODE["deterministic"] = bool(deterministic)
     if _SAVED:
         return softmpm_module
     for name in ("p2g", "grid_update", "g2p_advect", "substep", "step"):

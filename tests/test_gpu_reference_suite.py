@@ -8,8 +8,9 @@ imports that softmpm, calls paper_2402_01181_b200.install(softmpm) -- so
 softmpm.p2g / grid_update / g2p_advect / substep / step run on the B200
 kernels -- and maps the tests' fp64 tolerance literals (< 1e-5 on the right
 of a < / <= comparison or as an approx / allclose tolerance) to the fp32
-gate 1e-5.  The test runs that suite in a subprocess and requires every test
-to pass except the ones listed in EXPECTED_FAIL with the reason."""
+gate 1e-5.  The test runs that suite in a subprocess, in the fast mode and
+in the deterministic mode, and requires every test to pass except the ones
+listed in MAY_FAIL for that mode, with the reason.""" 
 import os
 import subprocess
 import sys
@@ -22,14 +23,23 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
 MODULES = ["test_transfers.py", "test_substep.py", "test_collision.py", "test_weights.py",
            "test_materials.py", "test_oracle.py"]
-# test id -> why it cannot hold for the fp32 drop-in (documented in DESIGN.md)
-EXPECTED_FAIL: dict[str, str] = {}
+# tests allowed to fail per install mode, with the reason (documented in DESIGN.md)
+_ORDER = ("fast mode flushes its fixed-point tiles into the grid with float L2 reductions in "
+          "arrival order, so runs agree to fp32 rounding, not bit for bit (SURVEY 8d: not required "
+          "in fast mode); install(deterministic=True) is bitwise reproducible")
+MAY_FAIL = {
+    "fast": {"test_substep.py::test_runs_are_bitwise_deterministic": _ORDER,
+             "test_substep.py::test_determinism_across_thread_counts": _ORDER},
+    "deterministic": {},
+}
 
 
 @pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "ref_tests")),
                     reason="reference not installed (bash tools/install_reference.sh)")
-def test_reference_hot_path_suite_through_install():
+@pytest.mark.parametrize("mode", ["fast", "deterministic"])
+def test_reference_hot_path_suite_through_install(mode):
     env = dict(os.environ)
+    env["SOFTMPM_INSTALL_DETERMINISTIC"] = "1" if mode == "deterministic" else "0"
     env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tools", "ref_suite"), REF, ROOT,
                                          env.get("PYTHONPATH", "")])
     env.setdefault("NUMBA_CACHE_DIR", "/tmp/softmpm_numba_cache")
@@ -40,9 +50,10 @@ def test_reference_hot_path_suite_through_install():
                        timeout=1200)
     out = r.stdout + r.stderr
     print(out[-8000:])
-    assert "install() active: True" in out
-    failed = [ln.split()[1] for ln in out.splitlines() if ln.startswith("FAILED ")]
-    failed = [f.split("::", 1)[1] if "::" in f else f for f in failed]
-    unexpected = [f for f in failed if f not in EXPECTED_FAIL]
+    assert "install() active: True" in out and f"install mode: {mode}" in out
+    failed = [ln.split()[1] for ln in out.splitlines() if ln.startswith(("FAILED ", "ERROR "))]
+    failed = [os.path.basename(f) for f in failed]
+    unexpected = [f for f in failed if f not in MAY_FAIL[mode]]
     assert not unexpected, unexpected
-    assert " passed" in out
+    passed = sum(1 for ln in out.splitlines() if ln.startswith("PASSED "))
+    assert passed >= 50, passed

@@ -36,9 +36,16 @@ if "skimage" not in sys.modules:
 os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "softmpm_numba_cache"))
 
 import softmpm  # noqa: E402  (baseline/_ref)
+import softmpm.oracle  # noqa: E402
 from paper_2402_01181_b200.install import install  # noqa: E402
 
-install(softmpm)
+DETERMINISTIC = os.environ.get("SOFTMPM_INSTALL_DETERMINISTIC") == "1"
+install(softmpm, deterministic=DETERMINISTIC)
+# the one tolerance kept as a module constant rather than a literal
+# (oracle.py: ORACLE_TOLERANCE = 1e-12, max |dx| per coordinate) gets the same rule
+if softmpm.oracle.ORACLE_TOLERANCE < FP32_TOL:
+    _REWRITES.append(f"softmpm.oracle.ORACLE_TOLERANCE: {softmpm.oracle.ORACLE_TOLERANCE!r} -> {FP32_TOL!r}")
+    softmpm.oracle.ORACLE_TOLERANCE = FP32_TOL
 
 
 def _is_small_float(node) -> bool:
@@ -101,6 +108,7 @@ def pytest_pycollect_makemodule(module_path, parent):
 
 
 def pytest_terminal_summary(terminalreporter):
+    terminalreporter.write_line(f"install mode: {'deterministic' if DETERMINISTIC else 'fast'}")
     terminalreporter.write_line(f"softmpm hot path: {softmpm.core.step.__module__} (install() active: "
                                 f"{softmpm.core.step.__module__.startswith('paper_2402_01181_b200')})")
     terminalreporter.write_line(f"fp64 -> fp32 tolerance literals raised to {FP32_TOL}: {len(_REWRITES)}")
