@@ -307,7 +307,19 @@ __device__ __forceinline__ void g2p_gather(const Params& p, const float x[3], fl
 
 // x += dt v, clamped to the margins of the particle's environment tile
 // (core.py:51-56, kernels.py:517-534; one tile = the whole grid normally).
+// SINGLE: one environment, no slab window (the common case, specialised at
+// compile time: no tile-origin arithmetic per particle and axis).
+template <bool SINGLE = false>
 __device__ __forceinline__ void advect(const Params& p, float x[3], const float v[3]) {
+  if constexpr (SINGLE) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float q = x[a] + p.dt * v[a];
+      q = q < p.lo ? p.lo : q;
+      q = q > p.hi[a] ? p.hi[a] : q;
+      x[a] = q;
+    }
+  } else {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     // environment tile origin in window-local coordinates (the walls keep a
@@ -320,6 +332,7 @@ __device__ __forceinline__ void advect(const Params& p, float x[3], const float 
     q = q < org + p.lo ? org + p.lo : q;
     q = q > org + p.hi[a] ? org + p.hi[a] : q;
     x[a] = q;
+  }
   }
 }
 
@@ -442,7 +455,7 @@ __device__ __forceinline__ void load_raw(const Params& p, long long i, PRaw<G2P>
 
 // Stage-A work for one slot: (G2P + advect) or (v, C as loaded), then F update
 // + stress -> payload.  STORE: write x and F back.  Returns det(F').
-template <bool G2P, bool STORE = true>
+template <bool G2P, bool STORE = true, bool SINGLE = false>
 __device__ __forceinline__ float compute_payload(const Params& p, long long i, PRaw<G2P>& r, Payload& q,
                                                  const TileVel* tv) {
   float v[3], C[9];
@@ -461,7 +474,7 @@ __device__ __forceinline__ float compute_payload(const Params& p, long long i, P
       if (tv) FPROF_COUNT(1);
       g2p_gather(p, global_vel(p), b, f, w, v, C);
     }
-    advect(p, r.x, v);
+    advect<SINGLE>(p, r.x, v);
     if (STORE) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) stf(p, FX + a, i, r.x[a]);
@@ -1036,6 +1049,7 @@ __device__ __forceinline__ long long fprof_clock_dep(int dep) {
 // The fused steady-state substep as a CTA-level phase (used by fused_kernel
 // and, once per substep, by the cooperative substeps_kernel).  zero_tile:
 // the int32 tile is cleared first (the flushes leave it clean afterwards).
+template <bool SINGLE>
 __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict__ bounds_in,
                                             float4* __restrict__ bounds_out, int* __restrict__ item_box,
                                             bool zero_tile, bool dep_wait = false) {
@@ -1104,7 +1118,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
       PRaw<true> r;
       load_raw<true>(p, i, r);
       Payload q;
-      const float det = compute_payload<true>(p, i, r, q, &tv);
+      const float det = compute_payload<true, true, SINGLE>(p, i, r, q, &tv);
       inverted += det <= 0.0f;
       float bnd[4];
       payload_bound(p, q, bnd);
@@ -1222,6 +1236,7 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
   warp_count_add(p.stats, guard);
 }
 
+template <bool SINGLE>
 __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kernel(Params p, float4* __restrict__ bounds_in,
                                                                                   float4* __restrict__ bounds_out,
                                                                                   int* __restrict__ item_box) {
@@ -1229,7 +1244,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS) fused_kerne
   const unsigned long long t0 = gtimer();
   if (threadIdx.x == 0) atomicMin(&g_bub[2], t0);
 #endif
-  fused_phase(p, bounds_in, bounds_out, item_box, true, true);
+  fused_phase<SINGLE>(p, bounds_in, bounds_out, item_box, true, true);
 #ifdef FUSED_PROFILE
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1523,7 +1538,7 @@ __global__ void __launch_bounds__(FUSED_K_THREADS, FUSED_MIN_BLOCKS)
       ctr[(t + 1) & 1] = 0;
       ctr[2 + ((t + 1) & 1)] = 0;
     }
-    fused_phase(q, bounds_in, bounds_out, item_box, t == 0);
+    fused_phase<false>(q, bounds_in, bounds_out, item_box, t == 0);
     float4* tmp = bounds_in;
     bounds_in = bounds_out;
     bounds_out = tmp;

@@ -581,7 +581,9 @@ int launch_fused(mpm_ctx* ctx, bool g2p) {
   ctx->bounds_out_clean = true;
   {
     TimedRegion tr(ctx, 5);
-    CK(launch_pdl(ctx, fused_kernel, ctx->fused_only_blocks, FUSED_K_THREADS, FUSED_SMEM, p,
+    const bool single = p.env_res[0] == p.gres[0] && p.env_res[1] == p.gres[1] && p.env_res[2] == p.gres[2] &&
+                        !p.goff[0] && !p.goff[1] && !p.goff[2];
+    CK(launch_pdl(ctx, single ? fused_kernel<true> : fused_kernel<false>, ctx->fused_only_blocks, FUSED_K_THREADS, FUSED_SMEM, p,
                   ctx->item_bounds, ctx->item_bounds2, ctx->item_box));
     LAUNCHED();
   }
@@ -775,7 +777,9 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
     size_t smem = P2G_SMEM;
-    cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(FUSED_SMEM));
+    cudaFuncSetAttribute(fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(FUSED_SMEM));
     {
       const char* e = getenv("SOFTMPM_SPLIT");
@@ -803,7 +807,7 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
     ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
-    ctx->fused_only_blocks = persistent((const void*)fused_kernel, FUSED_K_THREADS, FUSED_SMEM);
+    ctx->fused_only_blocks = persistent((const void*)fused_kernel<true>, FUSED_K_THREADS, FUSED_SMEM);
     cudaFuncSetAttribute(substeps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(FUSED_SMEM));
     ctx->mega_blocks = persistent((const void*)substeps_kernel, FUSED_K_THREADS, FUSED_SMEM);
