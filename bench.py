@@ -76,7 +76,7 @@ def _ncu_traffic(kernel_prefix: str, config: str):
         except Exception:
             continue
         for rec in d if isinstance(d, list) else [d]:
-            if str(rec.get("kernel", "")).startswith(kernel_prefix) and rec.get("dram_bytes"):
+            if kernel_prefix in str(rec.get("kernel", "")) and rec.get("dram_bytes"):
                 best = (rec["dram_bytes"], os.path.relpath(path, ROOT), rec.get("dram_bytes_warm"))
     return best
 

@@ -143,3 +143,44 @@ def test_encode_surface_frame_equals_host_encoding():
         sm.encode_frame(sm.extract_surface(st, 300.0, resolution=(32, 32, 32)), [], 1, 0.0)
     empty = sm.encode_surface_frame(st, 1e12, [], 3, 0.0)
     assert sm.decode_frame(empty).vertices.shape == (0, 3)
+
+
+# ---- parity against the CPU restatement of the Lorensen isosurface (oracle/mc_oracle.py)
+def _mc_oracle_compare(fld, iso):
+    from oracle import mc_oracle
+    mesh = sm.marching_cubes(fld, iso)
+    V, T, N = mc_oracle.marching_cubes(fld.values, iso, fld.dx)
+    # same vertex set, numbered alike (lattice-edge order), same positions / normals
+    assert mesh.vertices.shape == V.shape
+    assert np.abs(mesh.vertices - V).max() < 1e-12
+    assert np.abs(mesh.normals - N).max() < 1e-12
+    # same triangles, emitted in the same order (cube order, case-table order)
+    assert np.array_equal(mesh.indices, T)
+    return mesh
+
+
+def test_marching_cubes_matches_oracle_sphere():
+    fld, _ = sphere_field()
+    mesh = _mc_oracle_compare(fld, 300.0)
+    assert len(mesh.indices) > 500
+
+
+def test_marching_cubes_matches_oracle_random_fields(rng=np.random.default_rng(11)):
+    n = 18
+    for _ in range(3):
+        g = rng.normal(size=(n, n, n))
+        for axis in range(3):
+            g = (g + np.roll(g, 1, axis) + np.roll(g, -1, axis)) / 3.0
+        fld = sm.ScalarField(values=g - g.min() + 1e-3, dx=1.0 / n)
+        iso = float(np.median(fld.values))
+        _mc_oracle_compare(fld, iso)
+
+
+def test_marching_cubes_matches_oracle_splatted_state():
+    """The reference pipeline's own field: a settled block's B-spline splat."""
+    grid = sm.Grid(resolution=(20, 20, 20), extent=(1.0, 1.0, 1.0))
+    mats = [sm.Material(1.0e4, 0.3, 1000.0)]
+    spawn = sm.sample_box((0.5, 0.35, 0.5), (0.4, 0.3, 0.35), 6000, seed=8, grid=grid)
+    st = sm.SimState.from_spawns(grid, [spawn], mats)
+    sm.step(st, mats, sm.SimParams())
+    _mc_oracle_compare(sm.density_field(st), 300.0)

@@ -104,5 +104,46 @@ def launches(path):
     print(f"{'all':56s} {sum(a[0] for a in agg.values()):8d} {tot / 1e3:11.1f}")
 
 
+def warm(csv_path):
+    """Mean DRAM bytes per launch of each kernel in a warm-cache, no-replay
+    capture (`ncu --cache-control none --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file W.csv`)."""
+    rows = [r for r in csv.reader(open(csv_path)) if len(r) > 10]
+    hdr = rows[0]
+    ki, mi, ui, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
+    acc = collections.defaultdict(lambda: collections.defaultdict(list))
+    for r in rows[1:]:
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nsecond": 1e-3,
+                 "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
+        v = _f(r[vi])
+        if v is not None:
+            acc[r[ki]][r[mi]].append(v * scale)
+    out = {}
+    for k, m in acc.items():
+        rd, wr = m.get("dram__bytes_read.sum", []), m.get("dram__bytes_write.sum", [])
+        out[k] = {"launches": len(rd), "dram_bytes_warm": (sum(rd) + sum(wr)) / max(len(rd), 1),
+                  "duration_us_warm": sum(m.get("gpu__time_duration.sum", [])) / max(len(rd), 1)}
+    return out
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "full" and "--warm" in sys.argv:
+        # full X.ncu-rep --warm W.csv --config cN: one record with the warm DRAM bytes merged in
+        import io
+        from contextlib import redirect_stdout
+        buf = io.StringIO()
+        with redirect_stdout(buf):
+            full(sys.argv[2])
+        recs = json.loads(buf.getvalue())
+        recs = recs if isinstance(recs, list) else [recs]
+        w = warm(sys.argv[sys.argv.index("--warm") + 1])
+        cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else None
+        for rec in recs:
+            hit = [v for k, v in w.items() if k.split("(")[0].strip() in str(rec.get("kernel"))]
+            if hit:
+                rec.update(hit[0])
+            if cfg:
+                rec["config"] = cfg
+        print(json.dumps(recs[0] if len(recs) == 1 else recs, indent=1))
+    else:
+        {"full": full, "launches": launches, "warm": lambda p: print(json.dumps(warm(p), indent=1))}[sys.argv[1]](sys.argv[2])
