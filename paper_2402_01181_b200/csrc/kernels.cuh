@@ -1514,6 +1514,55 @@ __global__ void __launch_bounds__(256, GRIDOP_MIN_BLOCKS) grid_op_kernel(Params 
   }
 }
 
+// Grid op, plain form: one warp per active brick (two nodes per lane), no
+// software prefetch pipeline (2 CTAs of 8 warps per SM, the fp64 contact
+// chain out of line).  Same node math
+// (grid_node) and the same last-CTA counter reset as grid_op_kernel.
+#ifndef MPM_GRIDOP_SIMPLE_MINB
+#define MPM_GRIDOP_SIMPLE_MINB 2
+#endif
+__global__ void __launch_bounds__(256, MPM_GRIDOP_SIMPLE_MINB)
+    grid_op_simple_kernel(Params p, Colliders cs, int clear, int* done) {
+  __shared__ ColliderNearF nf_s[MAX_COLLIDERS];
+  const bool staged = !cs.per_env && cs.theta >= 0.0 && cs.count > 0 && cs.count <= MAX_COLLIDERS;
+  if (staged && threadIdx.x < cs.count) nf_s[threadIdx.x] = make_near_f(cs, threadIdx.x, cs.theta_f);
+  // collider tables come from the host: staged before the dependency wait (a
+  // no-op unless launched with programmatic dependent launch)
+  griddep_wait();
+  griddep_trigger();
+  const int lane = threadIdx.x & 31;
+  const long long nitems = *p.active_count;
+  __syncthreads();
+  const ColliderNearF* nf = staged ? nf_s : nullptr;
+  const bool single_env = p.env_res[0] == p.gres[0] && p.env_res[1] == p.gres[1] && p.env_res[2] == p.gres[2];
+  const double cap = 2.0 * cs.theta;
+  const int lj = (lane >> 2) & 3, lk = lane & 3, li0 = lane >> 4;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long it = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; it < nitems; it += nw) {
+    const long long b = p.active_list[it];
+    const long long i0 = (b << 6) | lane, i1 = i0 + 32;
+    const float4 a0 = p.gm[i0], a1 = p.gm[i1];
+    const unsigned t12 = p.fd_nb2.div((unsigned)b);
+    const int bk = (int)((unsigned)b - t12 * p.nb[2]);
+    const int bi = (int)p.fd_nb1.div(t12), bj = (int)t12 - bi * p.nb[1];
+    p.gv[i0] = grid_node(p, cs, nf, single_env, cap, a0, bi * 4 + li0, bj * 4 + lj, bk * 4 + lk);
+    p.gv[i1] = grid_node(p, cs, nf, single_env, cap, a1, bi * 4 + li0 + 2, bj * 4 + lj, bk * 4 + lk);
+    if (clear) {
+      p.gm[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      p.gm[i1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (lane == 0) p.brick_flag[b] = 0;
+  }
+  if (done) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      *p.active_count = 0;
+      *p.work_next = 0;
+      *done = 0;
+    }
+  }
+}
+
 // Substeps 2..L of a stretch in ONE cooperative launch: per substep the
 // fused phase (all items) and the grid-op phase (all active bricks),
 // separated by grid-wide barriers, so the kernel boundaries (launch, ramp,

@@ -149,6 +149,8 @@ struct mpm_ctx {
   float* mig_rows[2] = {nullptr, nullptr};
   long long mig_cap = 0;
   int gridop_blocks = 0;  // persistent grid sizes (SMs x resident CTAs)
+  int gridop_simple_blocks = 0;
+  bool gridop_simple = true;  // option "gridop_simple": warp-per-brick grid op (0 spills); 0 = the prefetching persistent kernel
   int gsA_blocks = 0, gsA0_blocks = 0, clear_blocks = 0, fused_only_blocks = 0;
 
   // optional per-kernel timing: event pairs per launch, resolved lazily
@@ -598,6 +600,8 @@ int launch_grid_op(mpm_ctx* ctx, bool dense, bool use_col, int row, bool clear) 
   int* done = clear && !dense ? ctx->counters + 63 : nullptr;  // counters reset by the last CTA
   if (dense)
     CK(launch_pdl(ctx, grid_op_kernel<true>, ctx->gridop_blocks, 256, 0, p, cs, clear ? 1 : 0, done));
+  else if (ctx->gridop_simple)
+    CK(launch_pdl(ctx, grid_op_simple_kernel, ctx->gridop_simple_blocks, 256, 0, p, cs, clear ? 1 : 0, done));
   else
     CK(launch_pdl(ctx, grid_op_kernel<false>, ctx->gridop_blocks, 256, 0, p, cs, clear ? 1 : 0, done));
   LAUNCHED();
@@ -803,6 +807,9 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     {
       const char* gb = getenv("SOFTMPM_GRIDOP_BLOCKS");  // CTAs per SM (A/B runs)
       ctx->gridop_blocks = ctx->sms * (gb && atoi(gb) > 0 ? atoi(gb) : GRIDOP_MIN_BLOCKS);
+      ctx->gridop_simple_blocks = persistent((const void*)grid_op_simple_kernel, 256, 0);
+      const char* gs = getenv("SOFTMPM_GRIDOP_SIMPLE");
+      if (gs) ctx->gridop_simple = gs[0] == '1';
     }
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
@@ -1360,6 +1367,9 @@ int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
   } else if (!strcmp(key, "pdl")) {
     invalidate_graphs(ctx);
     ctx->pdl_on = value != 0;
+  } else if (!strcmp(key, "gridop_simple")) {
+    invalidate_graphs(ctx);
+    ctx->gridop_simple = value != 0;
   } else if (!strcmp(key, "fx_shift")) {
     if (value < 0 || value > 8) return fail(ctx, MPM_EINVAL, "fx_shift: 0..8");
     invalidate_graphs(ctx);
