@@ -19,6 +19,7 @@ from . import core as _core
 from .collision import pack_colliders as _pack
 
 _SAVED: dict = {}
+_ABSENT = object()
 
 
 def _shadow(ref_state):
@@ -106,7 +107,7 @@ def install(softmpm_module, deterministic: bool = False):
     for name in ("p2g", "grid_update", "g2p_advect", "substep", "step"):
         _SAVED[name] = (getattr(core, name), getattr(softmpm_module, name, None))
     cls = core.SimState
-    _SAVED["__lazy__"] = (cls, {a: cls.__dict__.get(a) for a in ("grid_mv", "grid_m", "_collision")})
+    _SAVED["__lazy__"] = (cls, {a: cls.__dict__.get(a, _ABSENT) for a in ("grid_mv", "grid_m", "_collision")})
     for a in ("grid_mv", "grid_m", "_collision"):
         setattr(cls, a, _lazy_attr(a))
 
@@ -161,10 +162,10 @@ def uninstall(softmpm_module):
     core = softmpm_module.core
     cls, attrs = _SAVED.pop("__lazy__", (None, {}))
     for a, orig in attrs.items():
-        if orig is None:
+        if orig is _ABSENT:
             delattr(cls, a)
         else:
-            setattr(cls, a, orig)
+            setattr(cls, a, orig)  # e.g. the dataclass default _collision = None
     for name, (orig_core, orig_top) in _SAVED.items():
         setattr(core, name, orig_core)
         if orig_top is not None:

@@ -431,6 +431,8 @@ def split_state(grid: core.Grid, x, v, F, C, mass, vol0, mat, ranks: int, ghost_
     ids = np.arange(len(x), dtype=np.int32)
     for own in parts:
         sel = (base >= own[0]) & (base < own[1])
+        if not sel.any():
+            raise ParameterError(f"slab window {own} would start without particles")
         cap = int(max(16, capacity_factor * sel.sum() + 1024))
         wins.append(SlabWindow(grid, own, x[sel], v[sel], F[sel], C[sel], mass[sel], vol0[sel], mat[sel],
                                ids[sel], ghost_bricks=ghost_bricks, device=device, capacity=cap))

@@ -57,3 +57,49 @@ def test_reference_hot_path_suite_through_install(mode):
     assert not unexpected, unexpected
     passed = sum(1 for ln in out.splitlines() if ln.startswith("PASSED "))
     assert passed >= 50, passed
+
+
+def _import_reference():
+    import types
+    if "skimage" not in sys.modules:
+        sk = types.ModuleType("skimage")
+        sk.measure = types.ModuleType("skimage.measure")
+        sys.modules["skimage"], sys.modules["skimage.measure"] = sk, sk.measure
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/softmpm_numba_cache")
+    if REF not in sys.path:
+        sys.path.append(REF)
+    import softmpm
+    return softmpm
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "softmpm")),
+                    reason="reference not installed (bash tools/install_reference.sh)")
+def test_install_writes_back_collision_field_and_grid_lazily():
+    """install() on the real reference: after softmpm.step with a tool,
+    state._collision is the merged field of the last substep (core.py:307-309,
+    read by demos/02_tool_contact.py:39) and the dense grid arrives on first
+    read; uninstall() restores the class."""
+    import numpy as np
+    import paper_2402_01181_b200 as b200
+    ref = _import_reference()
+    had = "_collision" in ref.core.SimState.__dict__
+    b200.install(ref)
+    try:
+        grid = ref.Grid(resolution=(32, 32, 32), extent=(1.0, 1.0, 1.0))
+        mats = [ref.Material(1.0e4, 0.3, 1000.0)]
+        spawn = ref.sample_box((0.5, 0.14, 0.5), (0.3, 0.16, 0.3), 4000, seed=1, grid=grid)
+        st = ref.SimState.from_spawns(grid, [spawn], mats)
+        tool = ref.RigidCollider(id=0, shape=ref.Box(np.array([0.08, 0.03, 0.08])),
+                                 translation=np.array([0.5, 0.235, 0.5]),
+                                 linear_velocity=np.array([0.0, -0.5, 0.0]), friction_mu=0.4)
+        rep = ref.step(st, mats, ref.SimParams(), [tool])
+        assert rep.step_index == 1
+        assert "grid_mv" in st.__dict__.get("_b200_stale", set())   # not copied yet
+        col = st._collision
+        assert col is not None and (col.object_id >= 0).sum() > 0
+        assert col.distance.shape == grid.resolution
+        assert abs(st.grid_m.sum() - st.mass.sum()) < 1e-5 * st.mass.sum()
+        assert "grid_m" not in st.__dict__["_b200_stale"]
+    finally:
+        b200.uninstall(ref)
+    assert ("_collision" in ref.core.SimState.__dict__) == had
