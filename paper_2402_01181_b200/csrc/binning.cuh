@@ -15,9 +15,13 @@ namespace mpm {
 // shared-memory tile reads broadcast and int atomics hit few banks.
 __global__ void bin_key_kernel(Params p, int* key, int* lcell, int* rank, int* bin_count) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool valid = i < p.n;
+  // slots vacated by migrants (slab windows) are dropped by this re-binning
+  const bool valid = i < p.n && !(i < p.hole_n && p.hole_flag[i] != 0);
   const unsigned mask = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return;
+  if (!valid) {
+    if (i < p.n) key[i] = -1;
+    return;
+  }
   int c[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -40,7 +44,7 @@ __global__ void bin_key_kernel(Params p, int* key, int* lcell, int* rank, int* b
 __global__ void bin_fill_kernel(const int* key, const int* lcell, const int* rank, const int* start,
                                 int* sidx, int* slc, long long n) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || key[i] < 0) return;
   const int d = start[key[i]] + rank[i];
   sidx[d] = (int)i;
   slc[d] = lcell[i];

@@ -142,6 +142,10 @@ struct Params {
   // hook, default 0) scales the tile up by 2^fx_shift and the limit down
   unsigned long long* stats;
   int fx_shift;
+  // slab windows between a migrant extraction and the next re-binning:
+  // slots [0, hole_n) whose hole_flag is set have left (skipped by bin_key)
+  const int* hole_flag;
+  long long hole_n;
   // work items (bin, start, end, 0)
   const int4* work;
   const int* nwork;

@@ -75,6 +75,9 @@ struct mpm_ctx {
   int nmat = 0;
   unsigned long long* inverted = nullptr;
   unsigned long long* stats = nullptr;  // [0] fixed-point guard fallbacks (cumulative)
+  // slab windows: slots [0, hole_n) flagged in mflag have migrated away;
+  // hole_count of them; compacted by the next rebin (compact_if_needed)
+  long long hole_n = 0, hole_count = 0;
   int fx_shift = 0;                     // test hook: tile scale x 2^fx_shift, cell limit / 2^fx_shift
 
   // colliders
@@ -358,6 +361,8 @@ Params make_params(mpm_ctx* ctx) {
   p.inverted = ctx->inverted;
   p.stats = ctx->stats;
   p.fx_shift = ctx->fx_shift;
+  p.hole_flag = ctx->mflag;
+  p.hole_n = ctx->hole_n;
   p.work = ctx->work;
   p.nwork = ctx->counters + 1;
   p.work_next = ctx->counters + 3;
@@ -503,11 +508,15 @@ int rebin(mpm_ctx* ctx) {
                                                                 ctx->bin_maxcnt);
   LAUNCHED();
   int nxt = ctx->cur ^ 1;
-  gather_permute_kernel<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
+  const long long nvalid = ctx->n - ctx->hole_count;  // migrants' slots are dropped here
+  gather_permute_kernel<<<blocks_for(nvalid, 256), 256, 0, ctx->stream>>>(
       ctx->P[ctx->cur], ctx->mat[ctx->cur], ctx->orig[ctx->cur], ctx->P[nxt], ctx->mat[nxt], ctx->orig[nxt],
-      ctx->bperm, ctx->n, ctx->cap);
+      ctx->bperm, nvalid, ctx->cap);
   LAUNCHED();
   ctx->cur = nxt;
+  ctx->n = nvalid;
+  ctx->hole_n = 0;
+  ctx->hole_count = 0;
   // ~4 items per SM at least: small scenes split bins, large ones keep whole bins
   const int chunk = (int)std::max<long long>(MIN_CHUNK, std::min<long long>(CHUNK, ctx->n / ((long long)ctx->items_per_sm * ctx->sms)));
   static_assert(4 + 2 * WORK_CLASSES <= 64, "counters too small");
@@ -521,6 +530,13 @@ int rebin(mpm_ctx* ctx) {
   make_work_kernel<<<blocks_for(ctx->nbins, 256), 256, 0, ctx->stream>>>(
       ctx->bin_count, ctx->bin_start, ctx->bin_maxcnt, ctx->nbins, ctx->work, classes + WORK_CLASSES, chunk);
   LAUNCHED();
+  return 0;
+}
+
+// Slab windows: drop the slots of extracted migrants before anything reads
+// the particles in slot order (a re-binning compacts them).
+int compact_if_needed(mpm_ctx* ctx) {
+  if (ctx->hole_count > 0 || ctx->hole_n > 0) TRY(rebin(ctx));
   return 0;
 }
 
@@ -1036,6 +1052,7 @@ int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double
 int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, double* F, double* C) {
   if (!ctx || ctx->n <= 0) return fail(ctx, MPM_ESTATE, "download: no particles");
   CK(cudaSetDevice(ctx->dev));
+  TRY(compact_if_needed(ctx));
   long long n = ctx->n;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
   double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
@@ -1056,7 +1073,7 @@ int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, do
   return 0;
 }
 
-int64_t mpm_particle_count(mpm_ctx* ctx) { return ctx ? ctx->n : 0; }
+int64_t mpm_particle_count(mpm_ctx* ctx) { return ctx ? ctx->n - ctx->hole_count : 0; }
 
 int mpm_upload_grid(mpm_ctx* ctx, int target, const double* grid_mv, const double* grid_m) {
   if (!ctx || !grid_mv || (target != 0 && target != 1)) return fail(ctx, MPM_EINVAL, "upload_grid: bad arguments");
@@ -1412,6 +1429,7 @@ int mpm_collision_field(mpm_ctx* ctx, double theta, double* dist, int32_t* obj) 
 int mpm_has_nan(mpm_ctx* ctx, int* flag) {
   if (!ctx || !flag) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
+  TRY(compact_if_needed(ctx));
   *flag = 0;
   if (ctx->n <= 0) return 0;
   CK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
@@ -1426,6 +1444,7 @@ int mpm_has_nan(mpm_ctx* ctx, int* flag) {
 int mpm_metrics(mpm_ctx* ctx, const double* x0, double dx, double* out) {
   if (!ctx || !out) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
+  TRY(compact_if_needed(ctx));
   for (int k = 0; k < 5; ++k) out[k] = 0.0;
   out[4] = (double)ctx->n;
   if (ctx->n <= 0) return 0;
@@ -2044,6 +2063,7 @@ int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, in
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
   invalidate_graphs(ctx);
+  TRY(compact_if_needed(ctx));  // one extraction per re-binning
   const long long n = ctx->n;
   if (!ctx->mflag || ctx->mig_cap < ctx->cap) {
     TRY(dalloc(ctx, &ctx->mflag, (size_t)ctx->cap * 4));
@@ -2056,32 +2076,29 @@ int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, in
   Params p = make_params(ctx);
   migrant_flag_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, own_lo, own_hi, flag);
   LAUNCHED();
-  int totals[3] = {0, 0, 0};
-  int* posv[3];
-  // class scans reuse the key/rank/lcell scratch
-  posv[0] = ctx->key;
-  posv[1] = ctx->rank;
-  posv[2] = ctx->lcell;
-  for (int c = 0; c < 3; ++c) {
+  // ranks of the low / high migrants (class scans back to back, ONE host sync)
+  int* posv[3] = {nullptr, ctx->rank, ctx->lcell};  // class scans reuse the rank / lcell scratch
+  int last_pos[3] = {0, 0, 0}, last_cls[3] = {0, 0, 0};
+  for (int c = 1; c < 3 && n > 0; ++c) {
     flag_class_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(flag, c, cls, n);
     LAUNCHED();
     TRY(scan_exclusive(ctx, cls, posv[c], n));
-    int last_pos = 0, last_cls = 0;
-    CK(cudaMemcpyAsync(&last_pos, posv[c] + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&last_cls, cls + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    totals[c] = last_pos + last_cls;
+    CK(cudaMemcpyAsync(&last_pos[c], posv[c] + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&last_cls[c], cls + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   }
-  const int nxt = ctx->cur ^ 1;
-  migrant_scatter_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
-      p, flag, posv[0], posv[1], posv[2], ctx->P[nxt], ctx->mat[nxt], ctx->orig[nxt], ctx->mig_rows[0], ctx->mig_rows[1],
-      (long long)totals[1], (long long)totals[2]);
-  LAUNCHED();
   CK(cudaStreamSynchronize(ctx->stream));
-  ctx->cur = nxt;
-  ctx->n = totals[0];
-  if (n_lo) *n_lo = totals[1];
-  if (n_hi) *n_hi = totals[2];
+  const long long m_lo = last_pos[1] + last_cls[1], m_hi = last_pos[2] + last_cls[2];
+  if (m_lo + m_hi > 0) {
+    migrant_rows_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, flag, posv[1], posv[2], ctx->mig_rows[0],
+                                                                     ctx->mig_rows[1], m_lo, m_hi);
+    LAUNCHED();
+    CK(cudaStreamSynchronize(ctx->stream));
+    // the migrants' slots stay until the next re-binning drops them
+    ctx->hole_n = n;
+    ctx->hole_count = m_lo + m_hi;
+  }
+  if (n_lo) *n_lo = m_lo;
+  if (n_hi) *n_hi = m_hi;
   if (rows_lo) *rows_lo = ctx->mig_rows[0];
   if (rows_hi) *rows_hi = ctx->mig_rows[1];
   if (rows_cap) *rows_cap = 0;  // packed: each side's rows are a contiguous ROWS x count block
@@ -2098,9 +2115,13 @@ int mpm_append_particles(mpm_ctx* ctx, const void* rows, int64_t m, int64_t rows
   invalidate_graphs(ctx);
   Params p = make_params(ctx);
   const float dxs = (float)((src_offset - ctx->goff[0]) * ctx->cfg.dx);
+  // stream-ordered: the rows are complete (mpm_extract_migrants returns after
+  // its own stream synchronisation, peer rows arrive through a synchronised
+  // copy), and the caller's buffer must stay valid until this stream reaches
+  // the kernel (device buffers of the neighbour window / a torch tensor held
+  // until the next synchronisation)
   append_rows_kernel<<<blocks_for(m, 256), 256, 0, ctx->stream>>>(p, (const float*)rows, m, rows_cap, ctx->n, dxs);
   LAUNCHED();
-  CK(cudaStreamSynchronize(ctx->stream));
   ctx->n += m;
   return 0;
 }
@@ -2110,6 +2131,7 @@ int mpm_reserve(mpm_ctx* ctx, int64_t cap) {
   if (!ctx || cap <= ctx->cap) return 0;
   CK(cudaSetDevice(ctx->dev));
   invalidate_graphs(ctx);
+  TRY(compact_if_needed(ctx));
   float* P = nullptr;
   int *mat = nullptr, *orig = nullptr;
   TRY(dalloc(ctx, &P, (size_t)cap * NF));
@@ -2178,6 +2200,7 @@ int mpm_set_ids(mpm_ctx* ctx, const int32_t* ids) {
 int mpm_download_rows(mpm_ctx* ctx, int32_t* ids, double* x, double* v, double* F, double* C) {
   if (!ctx || !ids || !x || !v || !F || !C) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
+  TRY(compact_if_needed(ctx));
   const long long n = ctx->n;
   if (n <= 0) return 0;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 25 + 64));
@@ -2213,6 +2236,7 @@ int mpm_device_copy(void* dst, const void* src, int64_t bytes) {
 int mpm_download_ids(mpm_ctx* ctx, int32_t* ids, double* x) {
   if (!ctx || !ids || !x) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
+  TRY(compact_if_needed(ctx));
   const long long n = ctx->n;
   if (n <= 0) return 0;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 4 + 64));

@@ -165,31 +165,26 @@ __global__ void migrant_flag_kernel(Params p, int own_lo, int own_hi, int* flag)
   flag[i] = b < own_lo ? 1 : (b >= own_hi ? 2 : 0);
 }
 
-// Stable compaction by flag class via exclusive scans: dst row = pos[class][i].
-// Migrant rows are packed per side: field q of row d at out[q * m + d], m =
-// that side's migrant count (one contiguous ROWS x m block per neighbour).
-__global__ void migrant_scatter_kernel(Params p, const int* flag, const int* pos_keep, const int* pos_lo,
-                                       const int* pos_hi, float* keep_P, int* keep_mat, int* keep_orig,
-                                       float* out_lo, float* out_hi, long long m_lo, long long m_hi) {
+// Migrant rows (flag 1: low neighbour, 2: high neighbour) packed per side:
+// field q of row d at out[q * m + d], m = that side's migrant count (one
+// contiguous ROWS x m block per neighbour), d = the migrant's rank among its
+// side's migrants (exclusive scan).  The kept particles stay where they are:
+// their slots and the migrants' holes are compacted by the next re-binning
+// (bin_key_kernel skips flagged slots), so a stretch permutes the particle
+// state once, not twice.
+__global__ void migrant_rows_kernel(Params p, const int* flag, const int* pos_lo, const int* pos_hi, float* out_lo,
+                                    float* out_hi, long long m_lo, long long m_hi) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   const int f = flag[i];
-  if (f == 0) {
-    const long long d = pos_keep[i];
+  if (f == 0) return;
+  float* out = f == 1 ? out_lo : out_hi;
+  const long long d = f == 1 ? pos_lo[i] : pos_hi[i];
+  const long long out_cap = f == 1 ? m_lo : m_hi;
 #pragma unroll
-    for (int q = 0; q < NF; ++q) keep_P[q * p.cap + d] = ldf(p, q, i);
-    keep_mat[d] = p.mat[i];
-    keep_orig[d] = p.orig[i];
-  } else {
-    // row layout: NF floats, mat, orig (as float bits)
-    float* out = f == 1 ? out_lo : out_hi;
-    const long long d = f == 1 ? pos_lo[i] : pos_hi[i];
-    const long long out_cap = f == 1 ? m_lo : m_hi;
-#pragma unroll
-    for (int q = 0; q < NF; ++q) out[q * out_cap + d] = ldf(p, q, i);
-    out[NF * out_cap + d] = __int_as_float(p.mat[i]);
-    out[(NF + 1) * out_cap + d] = __int_as_float(p.orig[i]);
-  }
+  for (int q = 0; q < NF; ++q) out[q * out_cap + d] = ldf(p, q, i);
+  out[NF * out_cap + d] = __int_as_float(p.mat[i]);
+  out[(NF + 1) * out_cap + d] = __int_as_float(p.orig[i]);
 }
 
 __global__ void flag_class_kernel(const int* flag, int cls, int* out, long long n) {

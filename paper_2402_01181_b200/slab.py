@@ -346,9 +346,11 @@ class PeerExchange(LocalExchange):
     at all."""
 
     def __init__(self, windows):
+        from concurrent.futures import ThreadPoolExecutor
         super().__init__(windows)
         self.sides = []
         self.connected = False
+        self.pool = ThreadPoolExecutor(max_workers=len(windows))
 
     def connect(self):
         if self.connected:
@@ -393,20 +395,24 @@ def step_local_peer(windows, exchange: PeerExchange, materials, params, collider
                         c.call("mpm_stage_grid", sub, int(sub != nsub - 1))
                     elif sides[r]:
                         c.call("mpm_ipc_halo", phase, sides[r])
-        for c in ctxs:
-            inv = ctypes.c_int64()
-            c.call("mpm_stage_end", ctypes.byref(inv))
-            inverted += inv.value
-        outgoing = []
-        for win in windows:
-            nlo, nhi, plo, phi, cap = (ctypes.c_int64(), ctypes.c_int64(), _lib._VP(), _lib._VP(),
-                                       ctypes.c_int64())
-            win.state._ctx.call("mpm_extract_migrants", win.own[0], win.own[1], ctypes.byref(nlo),
-                                ctypes.byref(nhi), ctypes.byref(plo), ctypes.byref(phi), ctypes.byref(cap))
-            outgoing.append({0: (plo.value, nlo.value), 1: (phi.value, nhi.value)})
-        exchange.migrate(outgoing)
+        # stretch end, one host thread per window (the ctypes calls release the
+        # GIL): each window's final G2P, inverted count and migrant extraction
+        # synchronise only that window's stream, concurrently with the others
+        outgoing = list(exchange.pool.map(_stretch_end, windows))
+        inverted += sum(o[0] for o in outgoing)
+        exchange.migrate([o[1] for o in outgoing])
         s += span
     return inverted
+
+
+def _stretch_end(win):
+    c = win.state._ctx
+    inv = ctypes.c_int64()
+    c.call("mpm_stage_end", ctypes.byref(inv))
+    nlo, nhi, plo, phi, cap = (ctypes.c_int64(), ctypes.c_int64(), _lib._VP(), _lib._VP(), ctypes.c_int64())
+    c.call("mpm_extract_migrants", win.own[0], win.own[1], ctypes.byref(nlo), ctypes.byref(nhi),
+           ctypes.byref(plo), ctypes.byref(phi), ctypes.byref(cap))
+    return inv.value, {0: (plo.value, nlo.value), 1: (phi.value, nhi.value)}
 
 
 def gather(windows, n_total: int):
