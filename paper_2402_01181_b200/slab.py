@@ -569,7 +569,9 @@ def step_distributed(win: SlabWindow, ex, materials, params, colliders=None, pos
         ops_out = ex._sendrecv({nb: t.reshape(-1) for nb, t in send.items()},
                                {nb: (ROWS * got[nb],) for nb in got}, torch.float32)
         torch.cuda.synchronize()
-        offsets = ex.counts({nb: win.offset for nb in nbs.values()})
+        offsets = getattr(ex, "_nb_offsets", None)
+        if offsets is None:  # window offsets are fixed: exchanged once
+            offsets = ex._nb_offsets = ex.counts({nb: win.offset for nb in nbs.values()})
         for nb, t in ops_out.items():
             m = got[nb]
             if m:
