@@ -1212,7 +1212,10 @@ __device__ __forceinline__ void fused_phase(const Params& p, float4* __restrict_
 #else
     const float inv[4] = {1.0f / S[0], 1.0f / S[1], 1.0f / S[2], 1.0f / S[3]};
 #endif
-    flush_tile<4>(p, tile, org, x0, x1, y0, y1, z0, z1, inv, ccount);
+#ifndef MPM_FLUSH_SEG
+#define MPM_FLUSH_SEG 4
+#endif
+    flush_tile<MPM_FLUSH_SEG>(p, tile, org, x0, x1, y0, y1, z0, z1, inv, ccount);
     FPROF_MARK(tf);
     if (has_next) fused_item_scales(itn, nxt_bounds, scale_s[par ^ 1], p.fx_shift);
     cp_async_wait_all();
