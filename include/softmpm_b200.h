@@ -257,8 +257,10 @@ int mpm_get_timing(mpm_ctx *ctx, double *out);
  * cooperative kernel with grid barriers between the fused and grid-op
  * phases; pays off for small scenes, e.g. +12% at 30 K particles), "pdl"
  * (1 = fused kernel and grid op launched with programmatic dependent launch,
- * each kernel's prologue overlapping its predecessor's tail; off by default,
- * within noise at C3 and -0.4% at C4), "fx_shift" (test hook, 0..8: loosen
+ * each kernel's prologue overlapping its predecessor's tail; on by default:
+ * +1% at C3 with the plain grid op, within noise at C4 / C5), "gridop_simple"
+ * (1 = warp-per-brick grid op, the default; 0 = the prefetching persistent
+ * kernel), "fx_shift" (test hook, 0..8: loosen
  * the node-sum term of the fixed-point P2G scale by 2^value and divide the
  * per-cell count limit of its overflow guard by the same factor, so the
  * guard's float fallback is exercised on ordinary scenes; 0 in production). */

@@ -181,8 +181,8 @@ struct mpm_ctx {
   bool split_mode = false;  // SOFTMPM_SPLIT=1: stage A+B every substep (A/B comparison)
   int items_per_sm = 4;     // work-item granularity target (SOFTMPM_ITEMS_PER_SM)
   bool mega_on = false;   // substeps 2..L as one cooperative substeps_kernel (option "mega" / SOFTMPM_MEGA=1)
-  bool pdl_on = false;    // fused kernel / grid op with programmatic dependent launch (option "pdl" / SOFTMPM_PDL=1;
-                          // off by default: +-0.5% at C3, -0.4% at C4)
+  bool pdl_on = true;     // fused kernel / grid op with programmatic dependent launch (option "pdl" / SOFTMPM_PDL=0 to disable;
+                          // on by default: +1% at C3 with the plain grid op, within noise at C4 / C5)
   int mega_blocks = 0;
   bool mega_coop = false;  // device supports cooperative launches
   bool counters_clean = true;     // counters[0] (active bricks) and [3] (work_next) known zero
