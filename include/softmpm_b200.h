@@ -258,7 +258,11 @@ int mpm_get_timing(mpm_ctx *ctx, double *out);
  * phases; pays off for small scenes, e.g. +12% at 30 K particles), "pdl"
  * (1 = fused kernel and grid op launched with programmatic dependent launch,
  * each kernel's prologue overlapping its predecessor's tail; on by default:
- * +1% at C3 with the plain grid op, within noise at C4 / C5), "gridop_simple"
+ * +1% at C3 with the plain grid op, within noise at C4 / C5), "rebin_frames"
+ * (k >= 1: a frame of an untouched state keeps the particle order of a
+ * re-binning up to k - 1 frames old; default 1 -- k = 2 gains 1-1.6% on the
+ * settling C4 / C5 scenes but loses 7% on the pressed C3 slab, whose cells
+ * compress between re-binnings), "gridop_simple"
  * (1 = warp-per-brick grid op, the default; 0 = the prefetching persistent
  * kernel), "fx_shift" (test hook, 0..8: loosen
  * the node-sum term of the fixed-point P2G scale by 2^value and divide the

@@ -78,6 +78,10 @@ struct mpm_ctx {
   // slab windows: slots [0, hole_n) flagged in mflag have migrated away;
   // hole_count of them; compacted by the next rebin (compact_if_needed)
   long long hole_n = 0, hole_count = 0;
+  // cross-frame re-binning: frames since the last frame-start re-binning of
+  // an untouched state (-1: positions changed outside the fast path, re-bin)
+  int bins_age = -1;
+  int rebin_frames = 1;  // option "rebin_frames" / SOFTMPM_REBIN_FRAMES: re-bin every k-th frame (1 = every frame)
   int fx_shift = 0;                     // test hook: tile scale x 2^fx_shift, cell limit / 2^fx_shift
 
   // colliders
@@ -165,6 +169,7 @@ struct mpm_ctx {
   struct GraphEntry {
     int nsub, col, cur, border, dirty, timing;
     int prows;  // pose-table rows baked into the collider tables (make_colliders clamps row to prows - 1)
+    int skip;   // frame without its frame-start re-binning
     bool cclean, bclean;  // counters / bounds_out known zero at the start
     long long n;
     long long kernels;  // kernel nodes in the graph (evidence counter)
@@ -723,12 +728,17 @@ int read_inverted(mpm_ctx* ctx, int64_t* out) {
 }
 
 // The fast-path frame: re-binning + L-substep stretches (captured as a graph).
-int run_fast_sequence(mpm_ctx* ctx, int nsub, bool col) {
+// skip_rebin: the particles are still in the order of a re-binning at most
+// rebin_frames - 1 frames old and nothing outside the fast path moved them;
+// the frame keeps that order and work list (the first substep recomputes the
+// exact item bounds; particles that drifted off their tiles take the exact
+// float path).
+int run_fast_sequence(mpm_ctx* ctx, int nsub, bool col, bool skip_rebin = false) {
   TRY(ensure_gm_clean(ctx));
   int s = 0;
   while (s < nsub) {
     const int L = std::min(ctx->cfg.rebin_interval, nsub - s);
-    TRY(rebin(ctx));
+    if (!(skip_rebin && s == 0)) TRY(rebin(ctx));
     if (ctx->mega_on && L > 1) {
       TRY(launch_fused(ctx, false));
       TRY(launch_grid_op(ctx, false, col, s, s != nsub - 1));
@@ -826,6 +836,8 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
       ctx->gridop_simple_blocks = persistent((const void*)grid_op_simple_kernel, 256, 0);
       const char* gs = getenv("SOFTMPM_GRIDOP_SIMPLE");
       if (gs) ctx->gridop_simple = gs[0] == '1';
+      const char* rf = getenv("SOFTMPM_REBIN_FRAMES");
+      if (rf && atoi(rf) >= 1) ctx->rebin_frames = atoi(rf);
     }
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
@@ -937,6 +949,7 @@ int mpm_destroy(mpm_ctx* ctx) {
 }
 
 int mpm_set_config(mpm_ctx* ctx, const mpm_config* cfg) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || !cfg) return MPM_EINVAL;
   invalidate_graphs(ctx);
   std::string why;
@@ -973,6 +986,7 @@ int mpm_set_materials(mpm_ctx* ctx, const double* mu, const double* lam, int cou
 
 int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double* v, const double* F,
                          const double* C, const double* mass, const double* vol0, const int32_t* material_id) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || n <= 0 || !x || !v || !F || !C || !mass || !vol0 || !material_id)
     return fail(ctx, MPM_EINVAL, "upload_particles: bad arguments");
   if (n >= (1LL << 31) - CHUNK) return fail(ctx, MPM_EINVAL, "too many particles for one context");
@@ -1025,6 +1039,7 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
 
 int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double* v, const double* F,
                       const double* C) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || ctx->n <= 0) return fail(ctx, MPM_ESTATE, "upload_fields: no particles");
   if (!mask) return 0;
   CK(cudaSetDevice(ctx->dev));
@@ -1076,6 +1091,7 @@ int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, do
 int64_t mpm_particle_count(mpm_ctx* ctx) { return ctx ? ctx->n - ctx->hole_count : 0; }
 
 int mpm_upload_grid(mpm_ctx* ctx, int target, const double* grid_mv, const double* grid_m) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || !grid_mv || (target != 0 && target != 1)) return fail(ctx, MPM_EINVAL, "upload_grid: bad arguments");
   CK(cudaSetDevice(ctx->dev));
   long long nn = (long long)ctx->cfg.res[0] * ctx->cfg.res[1] * ctx->cfg.res[2];
@@ -1230,6 +1246,7 @@ int mpm_set_pose_table(mpm_ctx* ctx, int nsub, const double* rotation, const dou
 }
 
 int mpm_p2g(mpm_ctx* ctx, int64_t* inverted) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx) return MPM_EINVAL;
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
@@ -1248,6 +1265,7 @@ int mpm_p2g(mpm_ctx* ctx, int64_t* inverted) {
 }
 
 int mpm_grid_update(mpm_ctx* ctx, int use_colliders) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx) return MPM_EINVAL;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->grid_phase == 2) return fail(ctx, MPM_ESTATE, "grid holds velocities; run p2g first");
@@ -1259,6 +1277,7 @@ int mpm_grid_update(mpm_ctx* ctx, int use_colliders) {
 }
 
 int mpm_g2p(mpm_ctx* ctx) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx) return MPM_EINVAL;
   TRY(need_particles(ctx, false));  // g2p_advect (core.py:254-258) takes no materials
   CK(cudaSetDevice(ctx->dev));
@@ -1272,6 +1291,9 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
   bool col = use_colliders && ctx->ncol > 0 && ctx->cfg.theta >= 0.0;
+  // cross-frame re-binning (one stretch per frame only)
+  const bool skip = !ctx->cfg.deterministic && ctx->rebin_frames > 1 && ctx->cfg.rebin_interval >= nsub &&
+                    ctx->bins_age >= 0 && ctx->bins_age < ctx->rebin_frames;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(cudaMemsetAsync(ctx->inverted, 0, sizeof(unsigned long long), ctx->stream));
   if (ctx->cfg.deterministic) {
@@ -1282,7 +1304,7 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
     }
     ctx->grid_dirty = 2;
   } else if (!ctx->graphs_on) {
-    TRY(run_fast_sequence(ctx, nsub, col));
+    TRY(run_fast_sequence(ctx, nsub, col, skip));
   } else {
     const int border = ctx->item_bounds == ctx->bounds_a ? 0 : 1;
     const int timing = ctx->timing ? 1 : 0;
@@ -1291,7 +1313,8 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
     const int prows = col ? std::max(ctx->pose_rows, 1) : 0;
     mpm_ctx::GraphEntry* hit = nullptr;
     for (auto& g : ctx->graphs)
-      if (g.nsub == nsub && g.col == (int)col && g.prows == prows && g.cur == ctx->cur && g.border == border &&
+      if (g.nsub == nsub && g.col == (int)col && g.prows == prows && g.skip == (int)skip && g.cur == ctx->cur &&
+          g.border == border &&
           g.dirty == ctx->grid_dirty && g.timing == timing && g.n == ctx->n && g.cclean == ctx->counters_clean &&
           g.bclean == ctx->bounds_out_clean)
         hit = &g;
@@ -1300,6 +1323,7 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       e.nsub = nsub;
       e.col = (int)col;
       e.prows = prows;
+      e.skip = (int)skip;
       e.cur = ctx->cur;
       e.border = border;
       e.dirty = ctx->grid_dirty;
@@ -1310,7 +1334,7 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       const size_t marks0 = ctx->marks.size();
       const long long launches0 = ctx->launches;
       CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      const int rc = run_fast_sequence(ctx, nsub, col);
+      const int rc = run_fast_sequence(ctx, nsub, col, skip);
       cudaGraph_t graph = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
       if (rc || ce != cudaSuccess) {
@@ -1358,6 +1382,10 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
       for (auto& mk : hit->marks) ctx->marks.push_back(mk);
   }
   ctx->grid_phase = 1;
+  if (ctx->cfg.deterministic || ctx->cfg.rebin_interval < nsub)
+    ctx->bins_age = -1;
+  else
+    ctx->bins_age = skip ? ctx->bins_age + 1 : 1;
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   TRY(read_inverted(ctx, inverted));
   if (device_ms) {
@@ -1384,6 +1412,10 @@ int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
   } else if (!strcmp(key, "pdl")) {
     invalidate_graphs(ctx);
     ctx->pdl_on = value != 0;
+  } else if (!strcmp(key, "rebin_frames")) {
+    if (value < 1) return fail(ctx, MPM_EINVAL, "rebin_frames: >= 1");
+    ctx->rebin_frames = value;
+    ctx->bins_age = -1;
   } else if (!strcmp(key, "gridop_simple")) {
     invalidate_graphs(ctx);
     ctx->gridop_simple = value != 0;
@@ -1697,6 +1729,7 @@ int mpm_get_timing(mpm_ctx* ctx, double* out) {
 // ---- slab decomposition (BASELINE config 5) ----------------------------
 
 int mpm_set_slab(mpm_ctx* ctx, const int* global_res, const int* offset, int ghost_bricks) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || !global_res || !offset || ghost_bricks < 1) return fail(ctx, MPM_EINVAL, "set_slab: bad arguments");
   CK(cudaSetDevice(ctx->dev));
   for (int a = 0; a < 3; ++a) {
@@ -1962,6 +1995,7 @@ int mpm_halo_buffers(mpm_ctx* ctx, int side, void** send_ids, void** send_data, 
 }
 
 int mpm_stage_begin(mpm_ctx* ctx, int nsub, int use_colliders) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || nsub <= 0) return fail(ctx, MPM_EINVAL, "stage_begin: bad arguments");
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
@@ -2059,6 +2093,7 @@ int mpm_halo_unpack_vel(mpm_ctx* ctx, int side, int64_t n) {
 // pointers/capacity (rows: NF floats, material id, particle id; SoA by field).
 int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, int64_t* n_hi, void** rows_lo,
                          void** rows_hi, int64_t* rows_cap) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx) return MPM_EINVAL;
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
@@ -2108,6 +2143,7 @@ int mpm_extract_migrants(mpm_ctx* ctx, int own_lo, int own_hi, int64_t* n_lo, in
 // Append m migrant rows (device buffer in the layout above, capacity rows_cap)
 // coming from a window whose global x offset is src_offset nodes.
 int mpm_append_particles(mpm_ctx* ctx, const void* rows, int64_t m, int64_t rows_cap, int src_offset) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || m < 0) return MPM_EINVAL;
   if (m == 0) return 0;
   CK(cudaSetDevice(ctx->dev));
@@ -2128,6 +2164,7 @@ int mpm_append_particles(mpm_ctx* ctx, const void* rows, int64_t m, int64_t rows
 
 // Grow particle capacity (keeps contents) so migrants can be appended.
 int mpm_reserve(mpm_ctx* ctx, int64_t cap) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || cap <= ctx->cap) return 0;
   CK(cudaSetDevice(ctx->dev));
   invalidate_graphs(ctx);
@@ -2182,6 +2219,7 @@ int mpm_reserve(mpm_ctx* ctx, int64_t cap) {
 // Replace the original-index slot of every particle by ids[original index]
 // (slab windows carry global particle ids; field readback is then by id).
 int mpm_set_ids(mpm_ctx* ctx, const int32_t* ids) {
+  if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx || !ids) return MPM_EINVAL;
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
