@@ -20,8 +20,18 @@ __global__ void __launch_bounds__(METRICS_THREADS) metrics_kernel(Params p, cons
   for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n;
        s += (long long)gridDim.x * blockDim.x) {
     const long long id = p.orig[s];
-    const double d0 = (double)ldf(p, FX, s) - x0[3 * id], d1 = (double)ldf(p, FX + 1, s) - x0[3 * id + 1],
-                 d2 = (double)ldf(p, FX + 2, s) - x0[3 * id + 2];
+    // the device holds positions in fp32; a coordinate equal to the fp32
+    // rounding of x0 did not move (the host mirror keeps the caller's fp64
+    // value there, core.SimState._download), so its displacement is exactly
+    // zero, as scene.py:210-219 computes it on the host state
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float xa = ldf(p, FX + a, s);
+      const double x0a = x0[3 * id + a];
+      d[a] = xa == (float)x0a ? 0.0 : (double)xa - x0a;
+    }
+    const double d0 = d[0], d1 = d[1], d2 = d[2];
     c_lift += d1 > 2.0 * dx ? 1.0 : 0.0;
     c_det += d1 > dx ? 1.0 : 0.0;
     double F[9];

@@ -1,11 +1,14 @@
 """Route the reference package's hot path through the B200 kernels.
 
 ``install(softmpm)`` rebinds ``softmpm.core.p2g / grid_update / g2p_advect /
-substep / step`` (and the ``softmpm`` top-level re-exports) so unmodified
-callers -- ``cli.simulate`` (cli.py:71), ``cli.cmd_bench`` (cli.py:187-191),
-``server.Session.run_frame`` (server.py:407), ``oracle.oracle_divergence``,
-the demos -- run on the GPU while their ``SimState`` stays the reference's
-numpy dataclass.  Every call uploads the reference state's host arrays into a
+substep / step``, the surfacing consumers ``softmpm.surfacing.splat_density /
+marching_cubes / extract_surface`` and ``softmpm.scene.compute_metrics`` --
+every binding of them in the loaded package, including the copies that
+``from .core import step`` made in ``softmpm.cli`` and ``softmpm.server`` --
+so unmodified callers -- ``cli.simulate`` (cli.py:71), ``cli.cmd_bench``
+(cli.py:187-191), ``server.Session.run_frame`` (server.py:407),
+``oracle.oracle_divergence``, the demos -- run on the GPU while their
+``SimState`` stays the reference's numpy dataclass.  Every call uploads the reference state's host arrays into a
 device context cached on the state object and downloads the results back into
 those same arrays (the e2e host-buffer path).  ``uninstall()`` restores the
 originals.
@@ -13,9 +16,12 @@ originals.
 
 from __future__ import annotations
 
+import sys
+
 import numpy as np
 
 from . import core as _core
+from . import frame as _frame
 from .collision import pack_colliders as _pack
 
 _SAVED: dict = {}
@@ -43,6 +49,9 @@ def _shadow(ref_state):
 def _writeback(ref_state, sh, fields=("x", "v", "F", "C"), grid=True, collision=False):
     for nm in fields:
         np.copyto(getattr(ref_state, nm), getattr(sh, nm))
+    # the shadow's mirrors were only read (into the caller's own arrays): they
+    # still equal the device, so the next device call need not upload them
+    sh._host_dirty.difference_update(fields)
     d = ref_state.__dict__
     if grid:
         # the dense grid (537 MB at 256^3) is copied back only when read
@@ -104,8 +113,6 @@ def install(softmpm_module, deterministic: bool = False):
     _MODE["deterministic"] = bool(deterministic)
     if _SAVED:
         return softmpm_module
-    for name in ("p2g", "grid_update", "g2p_advect", "substep", "step"):
-        _SAVED[name] = (getattr(core, name), getattr(softmpm_module, name, None))
     cls = core.SimState
     _SAVED["__lazy__"] = (cls, {a: cls.__dict__.get(a, _ABSENT) for a in ("grid_mv", "grid_m", "_collision")})
     for a in ("grid_mv", "grid_m", "_collision"):
@@ -144,12 +151,68 @@ def install(softmpm_module, deterministic: bool = False):
         return softmpm_module.core.StepReport(rep.step_index, rep.sim_time, rep.timings_ms,
                                               rep.inverted_particles)
 
-    for name, fn in (("p2g", p2g), ("grid_update", grid_update), ("g2p_advect", g2p_advect),
-                     ("substep", substep), ("step", step)):
-        setattr(core, name, fn)
-        if hasattr(softmpm_module, name):
-            setattr(softmpm_module, name, fn)
+    # §8f consumers: the device splat / marching cubes / metrics, reading the
+    # shadow's device-resident particles when the caller's arrays still equal
+    # what the last step wrote back (no particle upload per frame)
+    surf = getattr(softmpm_module, "surfacing", None)
+    scene = getattr(softmpm_module, "scene", None)
+
+    def _ref_mesh(m):
+        return surf.SurfaceMesh(vertices=m.vertices, indices=np.asarray(m.indices, dtype=np.int32),
+                                uvs=m.uvs, normals=m.normals)
+
+    def splat_density(positions, masses, grid, resolution=None, chunks=8):
+        f = _frame.splat_density(positions, masses, _core.Grid(grid.resolution, grid.extent), resolution)
+        return surf.ScalarField(values=f.values, dx=f.dx)
+
+    def marching_cubes(fld, iso):
+        return _ref_mesh(_frame.marching_cubes(_frame.ScalarField(values=fld.values, dx=fld.dx), iso))
+
+    def extract_surface(state, iso, resolution=None):
+        sh = _synced_shadow(state, ("x",))
+        return _ref_mesh(_frame.extract_surface(sh, iso, resolution))
+
+    def compute_metrics(state, initial_positions):
+        sh = _synced_shadow(state, ("x", "F"))
+        m = _frame.compute_metrics(sh, initial_positions)
+        return scene.MetricSample(time=state.time, lifted_fraction=m.lifted_fraction,
+                                  detached_fraction=m.detached_fraction,
+                                  mean_abs_j_minus_1=m.mean_abs_j_minus_1, max_displacement=m.max_displacement)
+
+    new = {"p2g": p2g, "grid_update": grid_update, "g2p_advect": g2p_advect, "substep": substep, "step": step}
+    originals = {nm: getattr(core, nm) for nm in new}
+    if surf is not None:
+        for nm, fn in (("splat_density", splat_density), ("marching_cubes", marching_cubes),
+                       ("extract_surface", extract_surface)):
+            originals[nm], new[nm] = getattr(surf, nm), fn
+    if scene is not None and hasattr(scene, "compute_metrics"):
+        originals["compute_metrics"], new["compute_metrics"] = scene.compute_metrics, compute_metrics
+    # every binding of the originals in the loaded package -- softmpm.core.step,
+    # the softmpm.step re-export, and copies made by `from .core import step`
+    # in softmpm.cli / softmpm.server / ... -- is rebound (modules imported
+    # later pick up the patched core / surfacing attributes by themselves)
+    pkg = softmpm_module.__name__
+    rebound = []
+    for mname, mod in list(sys.modules.items()):
+        if mod is None or not (mname == pkg or mname.startswith(pkg + ".")):
+            continue
+        for nm, orig in originals.items():
+            if getattr(mod, nm, None) is orig:
+                setattr(mod, nm, new[nm])
+                rebound.append((mod, nm, orig))
+    _SAVED["__rebound__"] = rebound
     return softmpm_module
+
+
+def _synced_shadow(state, fields):
+    """The shadow state when the caller's arrays still hold what the last
+    installed call wrote back (compared in full), else a re-synchronised one."""
+    sh = state.__dict__.get("_b200_shadow")
+    if sh is not None and len(state.x) == sh.particle_count \
+            and all(f not in sh._host_dirty and f not in sh._dev_newer and np.array_equal(getattr(state, f), sh._h[f])
+                    for f in fields):
+        return sh
+    return _shadow(state)
 
 
 def _colliders(state, colliders):
@@ -159,17 +222,14 @@ def _colliders(state, colliders):
 
 
 def uninstall(softmpm_module):
-    core = softmpm_module.core
+    for mod, nm, orig in _SAVED.pop("__rebound__", []):
+        setattr(mod, nm, orig)
     cls, attrs = _SAVED.pop("__lazy__", (None, {}))
     for a, orig in attrs.items():
         if orig is _ABSENT:
             delattr(cls, a)
         else:
             setattr(cls, a, orig)  # e.g. the dataclass default _collision = None
-    for name, (orig_core, orig_top) in _SAVED.items():
-        setattr(core, name, orig_core)
-        if orig_top is not None:
-            setattr(softmpm_module, name, orig_top)
     _SAVED.clear()
 
 

@@ -22,15 +22,31 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
 MODULES = ["test_transfers.py", "test_substep.py", "test_collision.py", "test_weights.py",
-           "test_materials.py", "test_oracle.py"]
+           "test_materials.py", "test_oracle.py",
+           # the callers and data formats either side of the path: surfacing,
+           # scene build + metrics, the CLI, the acceptance suite, sampling, SDF, the server
+           "test_surfacing.py", "test_scene.py", "test_cli.py", "test_acceptance.py", "test_sampling.py",
+           "test_sdf.py", "test_server.py"]
 # tests allowed to fail per install mode, with the reason (documented in DESIGN.md)
 _ORDER = ("fast mode flushes its fixed-point tiles into the grid with float L2 reductions in "
           "arrival order, so runs agree to fp32 rounding, not bit for bit (SURVEY 8d: not required "
           "in fast mode); install(deterministic=True) is bitwise reproducible")
+_NOT_OURS = {
+    "test_server.py::test_golden_fixture_matches_current_encoder":
+        "the reference package ships frontend/test/fixtures/golden_frame.bin's generator outside pkg/src "
+        "(fails on the reference itself, SURVEY 4)",
+    "test_acceptance.py::test_sdf_fidelity_256":
+        "wall-clock budget of the reference's CPU numba SDF bake (off the hot path; 11.4 s vs 10 s on the "
+        "reference itself, SURVEY 4)",
+    "test_cli.py::test_multithread_not_slower_at_scale":
+        "times the reference's numba thread-count knob, which the GPU path does not use",
+}
 MAY_FAIL = {
     "fast": {"test_substep.py::test_runs_are_bitwise_deterministic": _ORDER,
-             "test_substep.py::test_determinism_across_thread_counts": _ORDER},
-    "deterministic": {},
+             "test_substep.py::test_determinism_across_thread_counts": _ORDER,
+             "test_server.py::test_session_pause_resume_reset": _ORDER + " (compares two sessions bit for bit)",
+             **_NOT_OURS},
+    "deterministic": dict(_NOT_OURS),
 }
 
 
@@ -47,7 +63,7 @@ def test_reference_hot_path_suite_through_install(mode):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-rA", "-p", "ref_suite_plugin",
                         "-p", "no:cacheprovider", "--rootdir", os.path.join(REF, "ref_tests"), *files],
                        cwd=os.path.join(REF, "ref_tests"), env=env, capture_output=True, text=True,
-                       timeout=1200)
+                       timeout=2400)
     out = r.stdout + r.stderr
     print(out[-8000:])
     assert "install() active: True" in out and f"install mode: {mode}" in out
@@ -56,7 +72,7 @@ def test_reference_hot_path_suite_through_install(mode):
     unexpected = [f for f in failed if f not in MAY_FAIL[mode]]
     assert not unexpected, unexpected
     passed = sum(1 for ln in out.splitlines() if ln.startswith("PASSED "))
-    assert passed >= 50, passed
+    assert passed >= 125, passed
 
 
 def _import_reference():

@@ -12,7 +12,7 @@ cp -r "$SRC" "$TMP/pkg"   # the build writes into the source tree; /root/referen
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target "$ROOT/baseline/_ref" --upgrade "$TMP/pkg"
 mkdir -p "$ROOT/baseline/_ref/ref_tests"
-for f in conftest.py test_transfers.py test_substep.py test_collision.py test_weights.py test_materials.py test_oracle.py; do
+for f in conftest.py test_transfers.py test_substep.py test_collision.py test_weights.py test_materials.py test_oracle.py test_surfacing.py test_scene.py test_cli.py test_acceptance.py test_sampling.py test_sdf.py test_server.py; do
   cp "$SRC/tests/$f" "$ROOT/baseline/_ref/ref_tests/$f"
 done
 rm -rf "$TMP"
