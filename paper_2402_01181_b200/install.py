@@ -17,6 +17,7 @@ originals.
 from __future__ import annotations
 
 import sys
+import types
 
 import numpy as np
 
@@ -192,10 +193,16 @@ def install(softmpm_module, deterministic: bool = False):
     # in softmpm.cli / softmpm.server / ... -- is rebound (modules imported
     # later pick up the patched core / surfacing attributes by themselves)
     pkg = softmpm_module.__name__
-    rebound = []
+    mods = {id(softmpm_module): softmpm_module}
+    for a in dir(softmpm_module):  # submodules reachable as attributes (also unregistered ones)
+        m = getattr(softmpm_module, a, None)
+        if isinstance(m, types.ModuleType):
+            mods.setdefault(id(m), m)
     for mname, mod in list(sys.modules.items()):
-        if mod is None or not (mname == pkg or mname.startswith(pkg + ".")):
-            continue
+        if mod is not None and (mname == pkg or mname.startswith(pkg + ".")):
+            mods.setdefault(id(mod), mod)
+    rebound = []
+    for mod in mods.values():
         for nm, orig in originals.items():
             if getattr(mod, nm, None) is orig:
                 setattr(mod, nm, new[nm])
