@@ -15,5 +15,9 @@ mkdir -p "$ROOT/baseline/_ref/ref_tests"
 for f in conftest.py test_transfers.py test_substep.py test_collision.py test_weights.py test_materials.py test_oracle.py test_surfacing.py test_scene.py test_cli.py test_acceptance.py test_sampling.py test_sdf.py test_server.py; do
   cp "$SRC/tests/$f" "$ROOT/baseline/_ref/ref_tests/$f"
 done
+mkdir -p "$ROOT/baseline/_ref/ref_demos"
+for f in 01_elastic_block.py 02_tool_contact.py 03_stiffness_sweep.py; do
+  cp "$SRC/demos/$f" "$ROOT/baseline/_ref/ref_demos/$f"
+done
 rm -rf "$TMP"
 echo "reference installed into $ROOT/baseline/_ref"
