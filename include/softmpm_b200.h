@@ -83,9 +83,18 @@ int mpm_set_materials(mpm_ctx *ctx, const double *mu, const double *lam, int cou
 int mpm_upload_particles(mpm_ctx *ctx, int64_t n, const double *x, const double *v,
                          const double *F, const double *C, const double *mass,
                          const double *vol0, const int32_t *material_id);
-/* Overwrite a subset of x/v/F/C (host-side edits of SimState fields). */
+/* Overwrite a subset of x/v/F/C (host-side edits of SimState fields).
+ * mask bits 0..3 select x, v, F, C (NULL pointers are skipped).  Pinned host
+ * buffers cross PCIe as fp64 and are converted on the device; pageable ones
+ * are narrowed to fp32 on host worker threads and cross as fp32 (option
+ * "host_xfer"; the same round-to-nearest values either way). */
 int mpm_upload_fields(mpm_ctx *ctx, uint32_t mask, const double *x, const double *v,
                       const double *F, const double *C);
+/* Download a subset of x/v/F/C in the caller's particle order.  mask bit 4
+ * (MPM_DOWNLOAD_KEEP_EQUAL): a destination value whose fp32 rounding equals
+ * the device value is left as it is (the device left it unchanged: the
+ * caller keeps its fp64 value), others get the device value. */
+#define MPM_DOWNLOAD_KEEP_EQUAL 16u
 int mpm_download_particles(mpm_ctx *ctx, uint32_t mask, double *x, double *v, double *F,
                            double *C);
 int64_t mpm_particle_count(mpm_ctx *ctx);
@@ -262,7 +271,10 @@ int mpm_get_timing(mpm_ctx *ctx, double *out);
  * (k >= 1: a frame of an untouched state keeps the particle order of a
  * re-binning up to k - 1 frames old; default 1 -- k = 2 gains 1-1.6% on the
  * settling C4 / C5 scenes but loses 7% on the pressed C3 slab, whose cells
- * compress between re-binnings), "gridop_simple"
+ * compress between re-binnings), "host_xfer" (1 = pageable host buffers of
+ * particle uploads / downloads are converted on host worker threads and
+ * cross PCIe as fp32, the default; 0 = always fp64 over PCIe with device
+ * conversion; SOFTMPM_HOST_THREADS sets the worker count), "gridop_simple"
  * (1 = warp-per-brick grid op, the default; 0 = the prefetching persistent
  * kernel), "fx_shift" (test hook, 0..8: loosen
  * the node-sum term of the fixed-point P2G scale by 2^value and divide the

@@ -22,6 +22,7 @@ _lib = None
 MPM_OK, MPM_EINVAL, MPM_ENOMEM, MPM_ECUDA, MPM_ESTATE, MPM_ESTENCIL = 0, -1, -2, -3, -4, -5
 FIELD_X, FIELD_V, FIELD_F, FIELD_C = 1, 2, 4, 8
 FIELD_ALL = 15
+DOWNLOAD_KEEP_EQUAL = 16  # MPM_DOWNLOAD_KEEP_EQUAL
 
 _D = ctypes.POINTER(ctypes.c_double)
 _I32 = ctypes.POINTER(ctypes.c_int32)

@@ -44,6 +44,7 @@ from .materials import Material, pack_materials
 
 _FIELDS = ("x", "v", "F", "C")
 _FIELD_BIT = {"x": _lib.FIELD_X, "v": _lib.FIELD_V, "F": _lib.FIELD_F, "C": _lib.FIELD_C}
+_KEEP_EQUAL = _lib.DOWNLOAD_KEEP_EQUAL
 
 
 @dataclass(frozen=True)
@@ -181,6 +182,19 @@ class SimState:
         self._h[name] = arr
         self._dev_newer.discard(name)
         self._host_dirty.add(name)
+
+    def _adopt(self, name: str, value) -> None:
+        """Take the caller's array itself as the host mirror of a field when it
+        already has the mirror's layout (C-contiguous, writeable fp64 of the
+        same shape): uploads read it and downloads land in it, no copy (the
+        drop-in's host-buffer path, install.py); else as _set."""
+        if (isinstance(value, np.ndarray) and value.dtype == np.float64 and value.flags.c_contiguous
+                and value.flags.writeable and value.shape == self._h[name].shape):
+            self._h[name] = value
+            self._dev_newer.discard(name)
+            self._host_dirty.add(name)
+        else:
+            self._set(name, value)
 
     x = property(lambda s: s._get("x"), lambda s, v: s._set("x", v))
     v = property(lambda s: s._get("v"), lambda s, v: s._set("v", v))
@@ -371,19 +385,18 @@ class SimState:
             for a, b in zip(snap, (self._mass, self._vol0, self._mat)))
 
     def _download(self, names) -> None:
-        mask = 0
+        mask = _KEEP_EQUAL
         for nm in names:
             mask |= _FIELD_BIT[nm]
-        fresh = {nm: np.empty_like(self._h[nm]) for nm in names}
+        # in place (callers may hold the arrays); the device holds fp32: where
+        # its value is the fp32 rounding of the host's last value (the kernels
+        # left it unchanged), the host's fp64 value is kept instead of the
+        # rounded one (e.g. G2P with a zero velocity field leaves x
+        # bit-identical, test_transfers.py:121) -- merged on the library's
+        # host threads (MPM_DOWNLOAD_KEEP_EQUAL)
         self._ctx.call("mpm_download_particles", ctypes.c_uint32(mask),
-                       *[_lib.ptr(fresh.get(nm)) for nm in _FIELDS])
+                       *[_lib.ptr(self._h[nm] if nm in names else None) for nm in _FIELDS])
         for nm in names:
-            # the device holds fp32: where its value is the fp32 rounding of
-            # the host's last value (the kernels left it unchanged), keep the
-            # host's fp64 value instead of the rounded one (e.g. G2P with a
-            # zero velocity field leaves x bit-identical, test_transfers.py:121)
-            old, new = self._h[nm], fresh[nm]
-            np.copyto(old, new, where=new != old.astype(np.float32))  # in place: callers may hold the array
             self._dev_newer.discard(nm)
 
     def _download_grid(self) -> None:

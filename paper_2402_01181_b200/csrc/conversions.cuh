@@ -40,6 +40,40 @@ __global__ void download_fields_kernel(Params p, double* __restrict__ x, double*
     for (int q = 0; q < 9; ++q) C[9 * o + q] = ldf(p, FC + q, s);
 }
 
+// The same with the host-converted fp32 wire format (mpm.cu host_xfer: the
+// caller's fp64 arrays are narrowed on host threads, exactly as the device's
+// round-to-nearest cvt would, and only fp32 crosses PCIe); unmasked fields
+// are null.
+__global__ void upload_fields32_kernel(Params p, const float* __restrict__ x, const float* __restrict__ v,
+                                       const float* __restrict__ F, const float* __restrict__ C) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= p.n) return;
+  long long o = p.orig[s];
+  if (x)
+    for (int a = 0; a < 3; ++a) stf(p, FX + a, s, x[3 * o + a]);
+  if (v)
+    for (int a = 0; a < 3; ++a) stf(p, FV + a, s, v[3 * o + a]);
+  if (F)
+    for (int q = 0; q < 9; ++q) stf(p, FF + q, s, F[9 * o + q]);
+  if (C)
+    for (int q = 0; q < 9; ++q) stf(p, FC + q, s, C[9 * o + q]);
+}
+
+__global__ void download_fields32_kernel(Params p, float* __restrict__ x, float* __restrict__ v,
+                                         float* __restrict__ F, float* __restrict__ C) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= p.n) return;
+  long long o = p.orig[s];
+  if (x)
+    for (int a = 0; a < 3; ++a) x[3 * o + a] = ldf(p, FX + a, s);
+  if (v)
+    for (int a = 0; a < 3; ++a) v[3 * o + a] = ldf(p, FV + a, s);
+  if (F)
+    for (int q = 0; q < 9; ++q) F[9 * o + q] = ldf(p, FF + q, s);
+  if (C)
+    for (int q = 0; q < 9; ++q) C[9 * o + q] = ldf(p, FC + q, s);
+}
+
 __global__ void upload_static_kernel(Params p, const double* mass, const double* vol, const int* mat) {
   long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= p.n) return;

@@ -9,7 +9,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +26,61 @@
 
 using namespace mpm;
 
+// Persistent host worker threads (the fp64 <-> fp32 conversions of the
+// particle transfers): run(f) calls f(thread, nthreads) on every worker and
+// the caller, and returns when all are done.
+struct HostPool {
+  explicit HostPool(int n) : nt(std::max(1, n)) {
+    for (int i = 1; i < nt; ++i) th.emplace_back([this, i] { loop(i); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> l(m);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+  }
+  void run(const std::function<void(int, int)>& f) {
+    {
+      std::lock_guard<std::mutex> l(m);
+      job = &f;
+      pending = nt - 1;
+      ++gen;
+    }
+    cv.notify_all();
+    f(0, nt);
+    std::unique_lock<std::mutex> l(m);
+    done_cv.wait(l, [&] { return pending == 0; });
+  }
+  int nt;
+
+ private:
+  void loop(int id) {
+    long long seen = 0;
+    for (;;) {
+      const std::function<void(int, int)>* j;
+      {
+        std::unique_lock<std::mutex> l(m);
+        cv.wait(l, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        j = job;
+      }
+      (*j)(id, nt);
+      std::lock_guard<std::mutex> l(m);
+      if (--pending == 0) done_cv.notify_one();
+    }
+  }
+  std::vector<std::thread> th;
+  std::mutex m;
+  std::condition_variable cv, done_cv;
+  const std::function<void(int, int)>* job = nullptr;
+  long long gen = 0;
+  int pending = 0;
+  bool stop = false;
+};
+
 struct mpm_ctx {
   mpm_config cfg{};
   int dev = 0;
@@ -28,6 +88,9 @@ struct mpm_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t xstream = nullptr;  // host<->device field copies, pipelined with the conversions
   cudaEvent_t field_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // host-converted particle transfers of pageable buffers (option
+  // "host_xfer", on by default; the workers are process-wide: XferShared)
+  bool host_xfer = true;
   std::string err;
   long long launches = 0;
 
@@ -756,6 +819,176 @@ int run_fast_sequence(mpm_ctx* ctx, int nsub, bool col, bool skip_rebin = false)
   return 0;
 }
 
+// ---- host-converted particle transfers -----------------------------------
+// The caller's fp64 AoS fields (pageable or pinned) are narrowed to fp32 on
+// host worker threads into pinned slots and only fp32 crosses PCIe (half the
+// bytes); downloads cross as fp32 and are widened on the host.  Each worker
+// owns a contiguous range of the masked fields' concatenated values and
+// pipelines its own slots (convert slot k while slot k^1 is in flight) on its
+// own copy stream.  Narrowing is (float)d, round to nearest even like the
+// device's cvt.rn.f32.f64; widening is exact: results are bit-identical to
+// the device-converted path.
+constexpr long long XFER_SLOT = 1 << 19;  // floats per pinned slot (2 MB)
+constexpr long long XFER_MIN = 1 << 20;   // values below which the calling thread converts alone
+
+// Process-wide transfer workers (contexts come and go: the reference's tests
+// build one per SimState): the thread pool, the pinned slots (portable), and
+// per device a copy stream and three events per worker.  Transfers of all
+// contexts are serialised on its mutex.  Never freed (idle threads at exit).
+struct XferShared {
+  std::mutex m;
+  HostPool* pool = nullptr;
+  float* slots = nullptr;
+  int nt = 0;
+  struct Dev {
+    int dev;
+    std::vector<cudaStream_t> st;
+    std::vector<cudaEvent_t> ev;  // 3 per worker: slot 0, slot 1, done
+  };
+  std::vector<Dev> devs;
+};
+XferShared& xfer_shared() {
+  static XferShared* g = new XferShared;
+  return *g;
+}
+
+// (called with the XferShared mutex held)
+int ensure_xfer(mpm_ctx* ctx, XferShared::Dev** out) {
+  XferShared& g = xfer_shared();
+  if (!g.pool) {
+    // (host memory bandwidth, not the thread count, bounds the conversions:
+    // 8 and 16 threads measure within 10% of each other on the B200 box)
+    int nt = (int)std::min<unsigned>(12u, std::max(1u, std::thread::hardware_concurrency()));
+    const char* e = getenv("SOFTMPM_HOST_THREADS");
+    if (e && atoi(e) > 0) nt = atoi(e);
+    void* h = nullptr;
+    CK(cudaHostAlloc(&h, sizeof(float) * XFER_SLOT * 2 * nt, cudaHostAllocPortable));
+    g.slots = static_cast<float*>(h);
+    g.nt = nt;
+    g.pool = new HostPool(nt);
+  }
+  for (auto& d : g.devs)
+    if (d.dev == ctx->dev) {
+      *out = &d;
+      return 0;
+    }
+  XferShared::Dev d;
+  d.dev = ctx->dev;
+  d.st.resize(g.nt);
+  d.ev.resize(3 * g.nt);
+  for (int t = 0; t < g.nt; ++t) {
+    CK(cudaStreamCreateWithFlags(&d.st[t], cudaStreamNonBlocking));
+    for (int k = 0; k < 3; ++k) CK(cudaEventCreateWithFlags(&d.ev[3 * t + k], cudaEventDisableTiming));
+  }
+  g.devs.push_back(std::move(d));
+  *out = &g.devs.back();
+  return 0;
+}
+
+struct XferSeg {
+  double* host;
+  long long count, voff;
+};
+
+// Pageable (not pinned / registered) host memory: DMA from it is staged by
+// the driver at a fraction of PCIe bandwidth.
+bool host_pageable(const void* ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Values [a, b) of the virtual (concatenated) field array: dir 0 narrows host
+// fp64 into dst, dir 1 widens src into host fp64.
+static void xfer_convert(const std::vector<XferSeg>& segs, long long a, long long b, float* slot, int dir,
+                         bool keep_equal) {
+  for (const XferSeg& g : segs) {
+    const long long lo = std::max(a, g.voff), hi = std::min(b, g.voff + g.count);
+    if (lo >= hi) continue;
+    double* hp = g.host + (lo - g.voff);
+    float* sp = slot + (lo - a);
+    const long long m = hi - lo;
+    if (dir == 0)
+      for (long long i = 0; i < m; ++i) sp[i] = (float)hp[i];
+    else if (keep_equal)
+      for (long long i = 0; i < m; ++i) {
+        if ((float)hp[i] != sp[i]) hp[i] = (double)sp[i];
+      }
+    else
+      for (long long i = 0; i < m; ++i) hp[i] = (double)sp[i];
+  }
+}
+
+// dir 0: host -> device stage; dir 1: device stage -> host.  `ready` is
+// recorded on ctx->stream before (the stage may be written / has been
+// written); the workers' completion is joined into ctx->stream (upload).
+int xfer_run(mpm_ctx* ctx, const std::vector<XferSeg>& segs, long long total, float* dstage, int dir,
+             cudaEvent_t ready, bool keep_equal = false) {
+  XferShared& g = xfer_shared();
+  std::lock_guard<std::mutex> guard(g.m);
+  XferShared::Dev* dv = nullptr;
+  TRY(ensure_xfer(ctx, &dv));
+  const int nrun = total < XFER_MIN ? 1 : g.nt;
+  std::atomic<int> err{0};
+  std::string msg;
+  std::mutex msg_m;
+  auto fn = [&](int t, int nt) {
+    auto ck = [&](cudaError_t e) {
+      if (e != cudaSuccess && !err.exchange(1)) {
+        std::lock_guard<std::mutex> l(msg_m);
+        msg = cudaGetErrorString(e);
+      }
+      return e == cudaSuccess;
+    };
+    if (!ck(cudaSetDevice(ctx->dev))) return;
+    const long long lo = total * t / nt, hi = total * (t + 1) / nt;
+    cudaStream_t st = dv->st[t];
+    float* slot[2] = {g.slots + XFER_SLOT * 2 * t, g.slots + XFER_SLOT * (2 * t + 1)};
+    cudaEvent_t ev[2] = {dv->ev[3 * t], dv->ev[3 * t + 1]};
+    if (!ck(cudaStreamWaitEvent(st, ready, 0))) return;
+    if (dir == 0) {
+      bool used[2] = {false, false};
+      int k = 0;
+      for (long long a = lo; a < hi; a += XFER_SLOT, k ^= 1) {
+        const long long b = std::min(a + XFER_SLOT, hi);
+        if (used[k] && !ck(cudaEventSynchronize(ev[k]))) return;  // the slot's last copy is done
+        xfer_convert(segs, a, b, slot[k], 0, false);
+        if (!ck(cudaMemcpyAsync(dstage + a, slot[k], sizeof(float) * (b - a), cudaMemcpyHostToDevice, st))) return;
+        if (!ck(cudaEventRecord(ev[k], st))) return;
+        used[k] = true;
+      }
+      ck(cudaEventRecord(dv->ev[3 * t + 2], st));
+    } else {
+      // copy of chunk j + 1 in flight while chunk j is widened
+      auto issue = [&](long long a, int k) {
+        const long long b = std::min(a + XFER_SLOT, hi);
+        return ck(cudaMemcpyAsync(slot[k], dstage + a, sizeof(float) * (b - a), cudaMemcpyDeviceToHost, st)) &&
+               ck(cudaEventRecord(ev[k], st));
+      };
+      if (lo < hi && !issue(lo, 0)) return;
+      int k = 0;
+      for (long long a = lo; a < hi; a += XFER_SLOT, k ^= 1) {
+        if (a + XFER_SLOT < hi && !issue(a + XFER_SLOT, k ^ 1)) return;
+        if (!ck(cudaEventSynchronize(ev[k]))) return;
+        xfer_convert(segs, a, std::min(a + XFER_SLOT, hi), slot[k], 1, keep_equal);
+      }
+    }
+  };
+  if (nrun == 1)
+    fn(0, 1);
+  else
+    g.pool->run(fn);
+  if (err.load()) return fail(ctx, MPM_ECUDA, "host transfer: " + msg);
+  if (dir == 0)
+    for (int t = 0; t < nrun; ++t) CK(cudaStreamWaitEvent(ctx->stream, dv->ev[3 * t + 2], 0));
+  if (dir == 0 && cudaStreamSynchronize(ctx->stream) != cudaSuccess)  // slots reusable once the copies are done
+    return fail(ctx, MPM_ECUDA, "host transfer: sync");
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -836,6 +1069,8 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
       ctx->gridop_simple_blocks = persistent((const void*)grid_op_simple_kernel, 256, 0);
       const char* gs = getenv("SOFTMPM_GRIDOP_SIMPLE");
       if (gs) ctx->gridop_simple = gs[0] == '1';
+      const char* hx = getenv("SOFTMPM_HOST_XFER");
+      if (hx) ctx->host_xfer = hx[0] == '1';
       const char* rf = getenv("SOFTMPM_REBIN_FRAMES");
       if (rf && atoi(rf) >= 1) ctx->rebin_frames = atoi(rf);
     }
@@ -1045,10 +1280,31 @@ int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double
   CK(cudaSetDevice(ctx->dev));
   long long n = ctx->n;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
-  double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
   const double* src[4] = {x, v, F, C};
   const int width[4] = {3, 3, 9, 9};
   Params p = make_params(ctx);
+  bool pageable = false;
+  for (int k = 0; k < 4; ++k)
+    if (((mask >> k) & 1u) && src[k]) pageable |= host_pageable(src[k]);
+  if (ctx->host_xfer && pageable) {
+    std::vector<XferSeg> segs;
+    float* f32[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* dst = reinterpret_cast<float*>(ctx->stage);
+    long long total = 0;
+    for (int k = 0; k < 4; ++k) {
+      if (!((mask >> k) & 1u) || !src[k]) continue;
+      segs.push_back({const_cast<double*>(src[k]), width[k] * n, total});
+      f32[k] = dst + total;
+      total += width[k] * n;
+    }
+    CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));  // stage buffer free
+    TRY(xfer_run(ctx, segs, total, dst, 0, ctx->field_ev[0]));
+    upload_fields32_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, f32[0], f32[1], f32[2], f32[3]);
+    LAUNCHED();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+  }
+  double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
   // field k's H2D copy (copy stream) overlaps field k-1's conversion
   CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));
   CK(cudaStreamWaitEvent(ctx->xstream, ctx->field_ev[0], 0));  // stage buffer free
@@ -1070,10 +1326,31 @@ int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, do
   TRY(compact_if_needed(ctx));
   long long n = ctx->n;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
-  double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
   double* dst[4] = {x, v, F, C};
   const int width[4] = {3, 3, 9, 9};
   Params p = make_params(ctx);
+  const bool keep_equal = (mask & MPM_DOWNLOAD_KEEP_EQUAL) != 0;
+  bool pageable = false;
+  for (int k = 0; k < 4; ++k)
+    if (((mask >> k) & 1u) && dst[k]) pageable |= host_pageable(dst[k]);
+  if (keep_equal || (ctx->host_xfer && pageable)) {
+    std::vector<XferSeg> segs;
+    float* f32[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* sb = reinterpret_cast<float*>(ctx->stage);
+    long long total = 0;
+    for (int k = 0; k < 4; ++k) {
+      if (!((mask >> k) & 1u) || !dst[k]) continue;
+      segs.push_back({dst[k], width[k] * n, total});
+      f32[k] = sb + total;
+      total += width[k] * n;
+    }
+    download_fields32_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, f32[0], f32[1], f32[2], f32[3]);
+    LAUNCHED();
+    CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));
+    TRY(xfer_run(ctx, segs, total, sb, 1, ctx->field_ev[0], keep_equal));
+    return 0;
+  }
+  double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};
   // field k's D2H copy (copy stream) overlaps field k+1's conversion
   for (int k = 0; k < 4; ++k) {
     if (!((mask >> k) & 1u) || !dst[k]) continue;
@@ -1416,6 +1693,8 @@ int mpm_set_option(mpm_ctx* ctx, const char* key, int value) {
     if (value < 1) return fail(ctx, MPM_EINVAL, "rebin_frames: >= 1");
     ctx->rebin_frames = value;
     ctx->bins_age = -1;
+  } else if (!strcmp(key, "host_xfer")) {
+    ctx->host_xfer = value != 0;
   } else if (!strcmp(key, "gridop_simple")) {
     invalidate_graphs(ctx);
     ctx->gridop_simple = value != 0;

@@ -30,7 +30,10 @@ _ABSENT = object()
 
 
 def _shadow(ref_state):
-    """Device-side SimState mirroring a reference SimState (same arrays by value)."""
+    """Device-side SimState mirroring a reference SimState: its x / v / F / C
+    mirrors ARE the reference state's arrays (SimState._adopt: uploads read
+    them, downloads land in them, no host copies), re-adopted and re-uploaded
+    on every call because the caller may have edited them in place."""
     sh = getattr(ref_state, "_b200_shadow", None)
     g = ref_state.grid
     if sh is None or sh.particle_count != len(ref_state.x):
@@ -39,9 +42,9 @@ def _shadow(ref_state):
                             ref_state.material_id)
         ref_state._b200_shadow = sh
     else:
-        for nm in ("x", "v", "F", "C"):
-            setattr(sh, nm, getattr(ref_state, nm))
         sh.mass, sh.vol0, sh.material_id = ref_state.mass, ref_state.vol0, ref_state.material_id
+    for nm in ("x", "v", "F", "C"):
+        sh._adopt(nm, getattr(ref_state, nm))
     sh.time = ref_state.time
     sh.step_count = ref_state.step_count
     return sh
@@ -49,7 +52,10 @@ def _shadow(ref_state):
 
 def _writeback(ref_state, sh, fields=("x", "v", "F", "C"), grid=True, collision=False):
     for nm in fields:
-        np.copyto(getattr(ref_state, nm), getattr(sh, nm))
+        src = getattr(sh, nm)  # the download (into the adopted array itself when it was adoptable)
+        dst = getattr(ref_state, nm)
+        if dst is not src:
+            np.copyto(dst, src)
     # the shadow's mirrors were only read (into the caller's own arrays): they
     # still equal the device, so the next device call need not upload them
     sh._host_dirty.difference_update(fields)
@@ -212,14 +218,15 @@ def install(softmpm_module, deterministic: bool = False):
 
 
 def _synced_shadow(state, fields):
-    """The shadow state when the caller's arrays still hold what the last
-    installed call wrote back (compared in full), else a re-synchronised one."""
+    """The shadow state with the fields a consumer reads re-adopted (and so
+    re-uploaded: the caller may have edited them in place since the last
+    installed call; one upload costs less than comparing the arrays)."""
     sh = state.__dict__.get("_b200_shadow")
-    if sh is not None and len(state.x) == sh.particle_count \
-            and all(f not in sh._host_dirty and f not in sh._dev_newer and np.array_equal(getattr(state, f), sh._h[f])
-                    for f in fields):
-        return sh
-    return _shadow(state)
+    if sh is None or len(state.x) != sh.particle_count:
+        return _shadow(state)
+    for f in fields:
+        sh._adopt(f, getattr(state, f))
+    return sh
 
 
 def _colliders(state, colliders):
