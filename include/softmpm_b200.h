@@ -84,10 +84,11 @@ int mpm_upload_particles(mpm_ctx *ctx, int64_t n, const double *x, const double 
                          const double *F, const double *C, const double *mass,
                          const double *vol0, const int32_t *material_id);
 /* Overwrite a subset of x/v/F/C (host-side edits of SimState fields).
- * mask bits 0..3 select x, v, F, C (NULL pointers are skipped).  Pinned host
- * buffers cross PCIe as fp64 and are converted on the device; pageable ones
- * are narrowed to fp32 on host worker threads and cross as fp32 (option
- * "host_xfer"; the same round-to-nearest values either way). */
+ * mask bits 0..3 select x, v, F, C (NULL pointers are skipped).  Pageable
+ * buffers and transfers of >= 2^20 values are narrowed to fp32 on host
+ * worker threads and cross PCIe as fp32; small pinned ones cross as fp64 and
+ * are converted on the device (option "host_xfer"; the same
+ * round-to-nearest values either way). */
 int mpm_upload_fields(mpm_ctx *ctx, uint32_t mask, const double *x, const double *v,
                       const double *F, const double *C);
 /* Download a subset of x/v/F/C in the caller's particle order.  mask bit 4
@@ -271,10 +272,11 @@ int mpm_get_timing(mpm_ctx *ctx, double *out);
  * (k >= 1: a frame of an untouched state keeps the particle order of a
  * re-binning up to k - 1 frames old; default 1 -- k = 2 gains 1-1.6% on the
  * settling C4 / C5 scenes but loses 7% on the pressed C3 slab, whose cells
- * compress between re-binnings), "host_xfer" (1 = pageable host buffers of
- * particle uploads / downloads are converted on host worker threads and
- * cross PCIe as fp32, the default; 0 = always fp64 over PCIe with device
- * conversion; SOFTMPM_HOST_THREADS sets the worker count), "gridop_simple"
+ * compress between re-binnings), "host_xfer" (1 = particle uploads /
+ * downloads of pageable buffers or >= 2^20 values are converted on host
+ * worker threads and cross PCIe as fp32, the default; 0 = always fp64 over
+ * PCIe with device conversion; SOFTMPM_HOST_THREADS sets the worker count,
+ * default min(16, hardware threads)), "gridop_simple"
  * (1 = warp-per-brick grid op, the default; 0 = the prefetching persistent
  * kernel), "fx_shift" (test hook, 0..8: loosen
  * the node-sum term of the fixed-point P2G scale by 2^value and divide the

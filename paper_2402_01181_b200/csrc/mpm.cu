@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <emmintrin.h>
 #include <cmath>
 #include <condition_variable>
 #include <functional>
@@ -91,6 +92,7 @@ struct mpm_ctx {
   // host-converted particle transfers of pageable buffers (option
   // "host_xfer", on by default; the workers are process-wide: XferShared)
   bool host_xfer = true;
+  bool xfer_direct = true;  // with pinned buffers x / v cross as fp64 beside it (SOFTMPM_XFER_DIRECT=0: off)
   std::string err;
   long long launches = 0;
 
@@ -856,9 +858,10 @@ XferShared& xfer_shared() {
 int ensure_xfer(mpm_ctx* ctx, XferShared::Dev** out) {
   XferShared& g = xfer_shared();
   if (!g.pool) {
-    // (host memory bandwidth, not the thread count, bounds the conversions:
-    // 8 and 16 threads measure within 10% of each other on the B200 box)
-    int nt = (int)std::min<unsigned>(12u, std::max(1u, std::thread::hardware_concurrency()));
+    // (1 M particles, 192 MB of fp64 each way, on the B200 box's 16 host
+    // threads: 8 workers 4.0 / 4.3 ms down / up, 12: 3.1 / 3.0, 16: 2.9 / 2.8;
+    // fp64 over PCIe with device conversion: 3.4 / 3.5)
+    int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
     const char* e = getenv("SOFTMPM_HOST_THREADS");
     if (e && atoi(e) > 0) nt = atoi(e);
     void* h = nullptr;
@@ -901,6 +904,48 @@ bool host_pageable(const void* ptr) {
   return a.type == cudaMemoryTypeUnregistered;
 }
 
+// fp64 -> fp32 into a pinned slot with streaming (non-temporal) stores: the
+// slot is read by the DMA engine right after, and a slot left dirty in the
+// CPU caches is read over PCIe at ~11 GB/s instead of ~55 (measured on the
+// B200 box's host); cvtpd2ps rounds to nearest even like (float)d.
+static void narrow_stream(const double* src, float* dst, long long m) {
+  long long i = 0;
+  for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) dst[i] = (float)src[i];
+  for (; i + 4 <= m; i += 4) {
+    const __m128 lo = _mm_cvtpd_ps(_mm_loadu_pd(src + i));
+    const __m128 hi = _mm_cvtpd_ps(_mm_loadu_pd(src + i + 2));
+    _mm_stream_ps(dst + i, _mm_movelh_ps(lo, hi));
+  }
+  for (; i < m; ++i) dst[i] = (float)src[i];
+  _mm_sfence();
+}
+
+// fp32 slot -> the caller's fp64 array with streaming stores (no read for
+// ownership of the destination lines).  keep_equal: a destination value
+// whose fp32 rounding equals the slot value is kept (MPM_DOWNLOAD_KEEP_EQUAL).
+static void widen_stream(const float* src, double* dst, long long m, bool keep_equal) {
+  long long i = 0;
+  auto one = [&](long long k) {
+    if (!keep_equal || (float)dst[k] != src[k]) dst[k] = (double)src[k];
+  };
+  for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) one(i);
+  for (; i + 2 <= m; i += 2) {
+    const __m128d w = _mm_cvtps_pd(_mm_castsi128_ps(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(src + i))));
+    if (keep_equal) {
+      const __m128d old = _mm_load_pd(dst + i);
+      // keep old where its fp32 rounding equals the new value (== on the
+      // fp32 values, so NaN never compares equal and -0 == +0 as in C)
+      const __m128 eq = _mm_cmpeq_ps(_mm_cvtpd_ps(old), _mm_cvtpd_ps(w));
+      const __m128d m2 = _mm_castps_pd(_mm_unpacklo_ps(eq, eq));
+      _mm_stream_pd(dst + i, _mm_or_pd(_mm_and_pd(m2, old), _mm_andnot_pd(m2, w)));
+    } else {
+      _mm_stream_pd(dst + i, w);
+    }
+  }
+  for (; i < m; ++i) one(i);
+  _mm_sfence();
+}
+
 // Values [a, b) of the virtual (concatenated) field array: dir 0 narrows host
 // fp64 into dst, dir 1 widens src into host fp64.
 static void xfer_convert(const std::vector<XferSeg>& segs, long long a, long long b, float* slot, int dir,
@@ -912,13 +957,9 @@ static void xfer_convert(const std::vector<XferSeg>& segs, long long a, long lon
     float* sp = slot + (lo - a);
     const long long m = hi - lo;
     if (dir == 0)
-      for (long long i = 0; i < m; ++i) sp[i] = (float)hp[i];
-    else if (keep_equal)
-      for (long long i = 0; i < m; ++i) {
-        if ((float)hp[i] != sp[i]) hp[i] = (double)sp[i];
-      }
+      narrow_stream(hp, sp, m);
     else
-      for (long long i = 0; i < m; ++i) hp[i] = (double)sp[i];
+      widen_stream(sp, hp, m, keep_equal);
   }
 }
 
@@ -1071,6 +1112,8 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
       if (gs) ctx->gridop_simple = gs[0] == '1';
       const char* hx = getenv("SOFTMPM_HOST_XFER");
       if (hx) ctx->host_xfer = hx[0] == '1';
+      const char* xd = getenv("SOFTMPM_XFER_DIRECT");
+      if (xd) ctx->xfer_direct = xd[0] == '1';
       const char* rf = getenv("SOFTMPM_REBIN_FRAMES");
       if (rf && atoi(rf) >= 1) ctx->rebin_frames = atoi(rf);
     }
@@ -1283,24 +1326,51 @@ int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double
   const double* src[4] = {x, v, F, C};
   const int width[4] = {3, 3, 9, 9};
   Params p = make_params(ctx);
+  // host-converted fp32 wire: pageable buffers (driver-staged DMA from them
+  // runs at ~11 GB/s) and every large transfer (host conversion on all
+  // threads beats the fp64 DMA); small pinned ones go as fp64
   bool pageable = false;
+  long long nval = 0;
   for (int k = 0; k < 4; ++k)
-    if (((mask >> k) & 1u) && src[k]) pageable |= host_pageable(src[k]);
-  if (ctx->host_xfer && pageable) {
+    if (((mask >> k) & 1u) && src[k]) {
+      pageable |= host_pageable(src[k]);
+      nval += width[k] * n;
+    }
+  if (ctx->host_xfer && (pageable || nval >= XFER_MIN)) {
+    // pinned buffers: x and v cross as fp64 straight from the caller's memory
+    // (device conversion) while the host threads narrow F and C, so PCIe and
+    // host memory bandwidth are both busy
+    const uint32_t direct = (!pageable && ctx->xfer_direct) ? (mask & 3u) : 0u;
+    double* st64 = ctx->stage;                                  // direct: x at 0, v at 3n
+    float* dst = reinterpret_cast<float*>(ctx->stage + 6 * n);  // fp32 wire after it
+    CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));  // stage buffer free
+    if (direct) {
+      CK(cudaStreamWaitEvent(ctx->xstream, ctx->field_ev[0], 0));
+      for (int k = 0; k < 2; ++k)
+        if (((direct >> k) & 1u) && src[k])
+          CK(cudaMemcpyAsync(st64 + 3 * n * k, src[k], sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->xstream));
+      CK(cudaEventRecord(ctx->field_ev[1], ctx->xstream));
+    }
     std::vector<XferSeg> segs;
     float* f32[4] = {nullptr, nullptr, nullptr, nullptr};
-    float* dst = reinterpret_cast<float*>(ctx->stage);
     long long total = 0;
     for (int k = 0; k < 4; ++k) {
-      if (!((mask >> k) & 1u) || !src[k]) continue;
+      if (!((mask >> k) & 1u) || !src[k] || ((direct >> k) & 1u)) continue;
       segs.push_back({const_cast<double*>(src[k]), width[k] * n, total});
       f32[k] = dst + total;
       total += width[k] * n;
     }
-    CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));  // stage buffer free
-    TRY(xfer_run(ctx, segs, total, dst, 0, ctx->field_ev[0]));
-    upload_fields32_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, f32[0], f32[1], f32[2], f32[3]);
-    LAUNCHED();
+    if (total) TRY(xfer_run(ctx, segs, total, dst, 0, ctx->field_ev[0]));
+    if (direct) {
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->field_ev[1], 0));
+      upload_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, st64, st64 + 3 * n, nullptr, nullptr,
+                                                                          direct);
+      LAUNCHED();
+    }
+    if (total) {
+      upload_fields32_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, f32[0], f32[1], f32[2], f32[3]);
+      LAUNCHED();
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     return 0;
   }
@@ -1330,24 +1400,43 @@ int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, do
   const int width[4] = {3, 3, 9, 9};
   Params p = make_params(ctx);
   const bool keep_equal = (mask & MPM_DOWNLOAD_KEEP_EQUAL) != 0;
-  bool pageable = false;
+  bool pageable = false;  // (as in mpm_upload_fields)
+  long long nval = 0;
   for (int k = 0; k < 4; ++k)
-    if (((mask >> k) & 1u) && dst[k]) pageable |= host_pageable(dst[k]);
-  if (keep_equal || (ctx->host_xfer && pageable)) {
+    if (((mask >> k) & 1u) && dst[k]) {
+      pageable |= host_pageable(dst[k]);
+      nval += width[k] * n;
+    }
+  if (keep_equal || (ctx->host_xfer && (pageable || nval >= XFER_MIN))) {
+    const uint32_t direct = (!pageable && !keep_equal && ctx->xfer_direct) ? (mask & 3u) : 0u;
+    double* st64 = ctx->stage;
+    float* sb = reinterpret_cast<float*>(ctx->stage + 6 * n);
+    if (direct) {
+      download_fields_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, st64, st64 + 3 * n, nullptr, nullptr,
+                                                                            direct);
+      LAUNCHED();
+      CK(cudaEventRecord(ctx->field_ev[1], ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->xstream, ctx->field_ev[1], 0));
+      for (int k = 0; k < 2; ++k)
+        if (((direct >> k) & 1u) && dst[k])
+          CK(cudaMemcpyAsync(dst[k], st64 + 3 * n * k, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->xstream));
+    }
     std::vector<XferSeg> segs;
     float* f32[4] = {nullptr, nullptr, nullptr, nullptr};
-    float* sb = reinterpret_cast<float*>(ctx->stage);
     long long total = 0;
     for (int k = 0; k < 4; ++k) {
-      if (!((mask >> k) & 1u) || !dst[k]) continue;
+      if (!((mask >> k) & 1u) || !dst[k] || ((direct >> k) & 1u)) continue;
       segs.push_back({dst[k], width[k] * n, total});
       f32[k] = sb + total;
       total += width[k] * n;
     }
-    download_fields32_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, f32[0], f32[1], f32[2], f32[3]);
-    LAUNCHED();
-    CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));
-    TRY(xfer_run(ctx, segs, total, sb, 1, ctx->field_ev[0], keep_equal));
+    if (total) {
+      download_fields32_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(p, f32[0], f32[1], f32[2], f32[3]);
+      LAUNCHED();
+      CK(cudaEventRecord(ctx->field_ev[0], ctx->stream));
+      TRY(xfer_run(ctx, segs, total, sb, 1, ctx->field_ev[0], keep_equal));
+    }
+    if (direct) CK(cudaStreamSynchronize(ctx->xstream));
     return 0;
   }
   double* st[4] = {ctx->stage, ctx->stage + 3 * n, ctx->stage + 6 * n, ctx->stage + 15 * n};

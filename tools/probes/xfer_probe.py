@@ -12,7 +12,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import paper_2402_01181_b200 as pk  # noqa: E402
 from paper_2402_01181_b200 import _lib, scenes  # noqa: E402
 
-st, mats, params, cols, pose_fn = scenes.c3()
+count = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+st, mats, params, cols, pose_fn = scenes.c3(count=count)
 pk.step(st, mats, params, cols, pose_fn)
 ctx = st._ctx
 L = _lib.lib()
@@ -39,7 +40,7 @@ for label, host in (("pinned", pinned), ("pageable", pageable)):
             t = time.perf_counter()
             ctx.call("mpm_upload_fields", ctypes.c_uint32(15), *args)
             tu.append(time.perf_counter() - t)
-        print(f"{label:9s} host_xfer={mode}: download {1e3 * min(td):.2f} ms ({mb / min(td) / 1e3:.1f} GB/s fp64), "
+        print(f"n={n} {label:9s} host_xfer={mode}: download {1e3 * min(td):.2f} ms ({mb / min(td) / 1e3:.1f} GB/s fp64), "
               f"upload {1e3 * min(tu):.2f} ms ({mb / min(tu) / 1e3:.1f} GB/s fp64)", flush=True)
 # host conversion alone (numpy, one thread) for scale
 a = pageable["F"]
