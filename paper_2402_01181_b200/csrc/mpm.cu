@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <functional>
 #include <mutex>
+#include <pthread.h>
 #include <thread>
 #include <cstdio>
 #include <cstdlib>
@@ -849,9 +850,16 @@ struct XferShared {
   };
   std::vector<Dev> devs;
 };
+XferShared* g_xfer = nullptr;
 XferShared& xfer_shared() {
-  static XferShared* g = new XferShared;
-  return *g;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    g_xfer = new XferShared;
+    // a forked child has none of the parent's worker threads (nor a usable
+    // CUDA context): it starts from an empty state instead of waiting on them
+    pthread_atfork(nullptr, nullptr, [] { g_xfer = new XferShared; });
+  });
+  return *g_xfer;
 }
 
 // (called with the XferShared mutex held)
