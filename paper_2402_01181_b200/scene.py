@@ -7,11 +7,11 @@ velocities are segment-constant, out-of-range times clamp with zero velocity,
 and closing a gripper group's jaws switches its members to sticky contact
 (which ``step`` then ignores in F7-compat mode, exactly like the reference).
 
-``pose_fn(colliders, t)`` is the only thing ``core.step`` needs; a PyBullet
-adapter would simply call ``RigidCollider.set_pose`` from
-``getBasePositionAndOrientation`` / ``getBaseVelocity`` inside one.  The
-reference's JSON scene schema and builtin scenario library are out of scope
-(host-side setup).
+``pose_fn(colliders, t)`` is the only thing ``core.step`` needs;
+``pybullet_pose_fn`` is one over a PyBullet simulation (the tools follow
+rigid bodies: ``getBasePositionAndOrientation`` / ``getBaseVelocity`` ->
+``RigidCollider.set_pose``, collision.py:74-82).  The reference's JSON scene
+schema and builtin scenario library are out of scope (host-side setup).
 """
 
 from __future__ import annotations
@@ -191,3 +191,24 @@ def make_pose_fn(trajectory: list[Keyframe], groups: list[GripperGroup] | None =
     if not trajectory:
         return None
     return PoseFn(trajectory, groups, base_mode)
+
+
+def pybullet_pose_fn(pb, body_ids, client=None):
+    """A ``pose_fn`` whose collider k follows PyBullet body ``body_ids[k]``:
+    base position / orientation (xyzw quaternion) give T and R, base linear /
+    angular velocity give the contact's rigid-motion velocity (kernels.py:
+    377-383).  ``pb`` is the ``pybullet`` module (or anything with its two
+    functions); PyBullet owns the clock, so the substep time is not used --
+    step the rigid-body world between frames, or every substep from a
+    pose_fn that wraps this one.  Each call reads every body once."""
+    kw = {} if client is None else {"physicsClientId": client}
+
+    def pose_fn(colliders, t):
+        for c, b in zip(colliders, body_ids):
+            pos, orn = pb.getBasePositionAndOrientation(b, **kw)
+            lin, ang = pb.getBaseVelocity(b, **kw)
+            c.set_pose(Rotation.from_quat(np.asarray(orn, dtype=np.float64)).as_matrix(),
+                       np.asarray(pos, dtype=np.float64), lin, ang)
+
+    return pose_fn
+
