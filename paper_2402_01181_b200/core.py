@@ -345,8 +345,6 @@ class SimState:
             return  # slab windows own their particle set on the device (migration)
         ctx = self._ctx
         n = len(self._h["x"])
-        if n == 0:
-            raise ParameterError("SimState has no particles")
         if self._static_dirty and int(_lib.lib().mpm_particle_count(ctx.h)) == n and self._static_same():
             # a read of mass / vol0 / material_id (the getter cannot know whether
             # the caller wrote into the array) that left them unchanged

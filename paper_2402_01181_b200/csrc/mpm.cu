@@ -109,6 +109,7 @@ struct mpm_ctx {
 
   // particles (double-buffered SoA)
   long long n = 0, cap = 0;
+  bool uploaded = false;  // a particle set (possibly empty) was uploaded
   float* P[2] = {nullptr, nullptr};
   int* mat[2] = {nullptr, nullptr};
   int* orig[2] = {nullptr, nullptr};
@@ -777,10 +778,21 @@ int det_p2g(mpm_ctx* ctx) {
   return 0;
 }
 
+// An uploaded empty particle set (not a slab window, whose set migrates).
+bool empty_state(const mpm_ctx* ctx) { return ctx->n == 0 && ctx->uploaded && ctx->h_cap == 0; }
+
+int zero_grid(mpm_ctx* ctx) {
+  CK(cudaMemsetAsync(ctx->gm, 0, sizeof(float4) * ctx->nbricks * 64, ctx->stream));
+  CK(cudaMemsetAsync(ctx->brick_flag, 0, sizeof(int) * ctx->nbricks, ctx->stream));
+  ctx->grid_dirty = 0;
+  return 0;
+}
+
 int need_particles(mpm_ctx* ctx, bool materials = true) {
   // a slab window may run empty after migration (it still takes part in the
   // halo protocol and can receive migrants): only its capacity must exist
-  if (ctx->n <= 0 && !(ctx->h_cap > 0 && ctx->cap > 0)) return fail(ctx, MPM_ESTATE, "no particles uploaded");
+  if (ctx->n <= 0 && !ctx->uploaded && !(ctx->h_cap > 0 && ctx->cap > 0))
+    return fail(ctx, MPM_ESTATE, "no particles uploaded");
   if (materials && ctx->nmat <= 0) return fail(ctx, MPM_ESTATE, "no materials set");
   return 0;
 }
@@ -1273,8 +1285,17 @@ int mpm_set_materials(mpm_ctx* ctx, const double* mu, const double* lam, int cou
 int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double* v, const double* F,
                          const double* C, const double* mass, const double* vol0, const int32_t* material_id) {
   if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
-  if (!ctx || n <= 0 || !x || !v || !F || !C || !mass || !vol0 || !material_id)
+  if (!ctx || n < 0 || (n > 0 && (!x || !v || !F || !C || !mass || !vol0 || !material_id)))
     return fail(ctx, MPM_EINVAL, "upload_particles: bad arguments");
+  if (n == 0) {
+    // an empty state (the reference steps it: grid ops on an empty grid, the
+    // clock advances): nothing to allocate, every particle stage a no-op
+    invalidate_graphs(ctx);
+    ctx->n = 0;
+    ctx->cur = 0;
+    ctx->uploaded = true;
+    return 0;
+  }
   if (n >= (1LL << 31) - CHUNK) return fail(ctx, MPM_EINVAL, "too many particles for one context");
   for (int64_t i = 0; i < n; ++i)
     if (material_id[i] < 0 || (ctx->nmat > 0 && material_id[i] >= ctx->nmat))
@@ -1312,6 +1333,7 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
   }
   ctx->n = n;
   ctx->cur = 0;
+  ctx->uploaded = true;
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
   double* s = ctx->stage;
   CK(cudaMemcpyAsync(s, mass, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -1326,7 +1348,8 @@ int mpm_upload_particles(mpm_ctx* ctx, int64_t n, const double* x, const double*
 int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double* v, const double* F,
                       const double* C) {
   if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
-  if (!ctx || ctx->n <= 0) return fail(ctx, MPM_ESTATE, "upload_fields: no particles");
+  if (!ctx) return MPM_EINVAL;
+  if (ctx->n <= 0) return ctx->uploaded ? 0 : fail(ctx, MPM_ESTATE, "upload_fields: no particles");
   if (!mask) return 0;
   CK(cudaSetDevice(ctx->dev));
   long long n = ctx->n;
@@ -1399,7 +1422,8 @@ int mpm_upload_fields(mpm_ctx* ctx, uint32_t mask, const double* x, const double
 }
 
 int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, double* F, double* C) {
-  if (!ctx || ctx->n <= 0) return fail(ctx, MPM_ESTATE, "download: no particles");
+  if (!ctx) return MPM_EINVAL;
+  if (ctx->n <= 0 && ctx->h_cap == 0) return ctx->uploaded ? 0 : fail(ctx, MPM_ESTATE, "download: no particles");
   CK(cudaSetDevice(ctx->dev));
   TRY(compact_if_needed(ctx));
   long long n = ctx->n;
@@ -1625,6 +1649,11 @@ int mpm_p2g(mpm_ctx* ctx, int64_t* inverted) {
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
   CK(cudaMemsetAsync(ctx->inverted, 0, sizeof(unsigned long long), ctx->stream));
+  if (empty_state(ctx)) {
+    TRY(zero_grid(ctx));
+    ctx->grid_phase = 0;
+    return read_inverted(ctx, inverted);
+  }
   if (ctx->cfg.deterministic) {
     TRY(det_p2g(ctx));
   } else {
@@ -1654,6 +1683,7 @@ int mpm_g2p(mpm_ctx* ctx) {
   if (ctx) ctx->bins_age = -1;  // particle order / positions may change: the next frame re-bins
   if (!ctx) return MPM_EINVAL;
   TRY(need_particles(ctx, false));  // g2p_advect (core.py:254-258) takes no materials
+  if (empty_state(ctx)) return 0;
   CK(cudaSetDevice(ctx->dev));
   TRY(launch_g2p(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1664,6 +1694,17 @@ int mpm_substeps(mpm_ctx* ctx, int nsub, int use_colliders, int64_t* inverted, d
   if (!ctx || nsub <= 0) return fail(ctx, MPM_EINVAL, "substeps: nsub must be >= 1");
   TRY(need_particles(ctx));
   CK(cudaSetDevice(ctx->dev));
+  if (empty_state(ctx)) {
+    // no particles: every substep's P2G leaves the grid empty and the grid op
+    // keeps massless nodes as they are (kernels.py:364-365)
+    TRY(zero_grid(ctx));
+    ctx->grid_phase = 1;
+    ctx->bins_age = -1;
+    if (inverted) *inverted = 0;
+    if (device_ms) *device_ms = 0.0;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+  }
   bool col = use_colliders && ctx->ncol > 0 && ctx->cfg.theta >= 0.0;
   // cross-frame re-binning (one stretch per frame only)
   const bool skip = !ctx->cfg.deterministic && ctx->rebin_frames > 1 && ctx->cfg.rebin_interval >= nsub &&
