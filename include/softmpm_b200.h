@@ -79,7 +79,9 @@ const char *mpm_version(void);
 /* ---- materials: replaces materials.pack_materials (materials.py:77-82) --- */
 int mpm_set_materials(mpm_ctx *ctx, const double *mu, const double *lam, int count);
 
-/* ---- particle state: SimState x/v/F/C/mass/vol0/material_id (core.py:92-143) */
+/* ---- particle state: SimState x/v/F/C/mass/vol0/material_id (core.py:92-143)
+ * n = 0 is a valid (empty) state, as in the reference: substeps then run the
+ * grid stages on an empty grid and particle transfers are no-ops. */
 int mpm_upload_particles(mpm_ctx *ctx, int64_t n, const double *x, const double *v,
                          const double *F, const double *C, const double *mass,
                          const double *vol0, const int32_t *material_id);
