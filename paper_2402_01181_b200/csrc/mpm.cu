@@ -1427,6 +1427,7 @@ int mpm_download_particles(mpm_ctx* ctx, uint32_t mask, double* x, double* v, do
   CK(cudaSetDevice(ctx->dev));
   TRY(compact_if_needed(ctx));
   long long n = ctx->n;
+  if (n <= 0) return 0;  // (a slab window that currently owns no particles)
   TRY(ensure_stage(ctx, sizeof(double) * (size_t)n * 24));
   double* dst[4] = {x, v, F, C};
   const int width[4] = {3, 3, 9, 9};
