@@ -51,6 +51,9 @@ def _shadow(ref_state):
 
 
 def _writeback(ref_state, sh, fields=("x", "v", "F", "C"), grid=True, collision=False):
+    newer = tuple(nm for nm in fields if nm in sh._dev_newer)
+    if newer:
+        sh._download(newer)  # one transfer for all of them
     for nm in fields:
         src = getattr(sh, nm)  # the download (into the adopted array itself when it was adoptable)
         dst = getattr(ref_state, nm)
