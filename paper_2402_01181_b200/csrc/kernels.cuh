@@ -1286,6 +1286,51 @@ __global__ void __launch_bounds__(256) g2p_kernel(Params p) {
   for (int q = 0; q < 9; ++q) stf(p, FC + q, i, C[q]);
 }
 
+// Final G2P of a fast-path stretch, one work item at a time: the item's
+// velocity tile (the node box its particles scattered to in the stretch's
+// last substep, item_box) is staged in shared memory with LDGSTS and the
+// gathers read it (the global grid for a particle outside it), then advect
+// and x / v / C.  Same sums in the same order as g2p_kernel.
+template <bool SINGLE>
+__global__ void __launch_bounds__(256) g2p_tile_kernel(Params p, const int* __restrict__ item_box) {
+  extern __shared__ float smem[];
+  const int nwork = *p.nwork;
+  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const int4 item = p.work[wi];
+    TileVel tv;
+    tv.t = smem;
+    fused_item_geometry(p, item, item_box[wi], tv);
+    __syncthreads();  // the previous item's gathers are done with the tile
+    fused_item_vtile_issue(p, tv, smem);
+    cp_async_wait_all();
+    __syncthreads();
+    for (long long i = (long long)item.y + threadIdx.x; i < item.z; i += blockDim.x) {
+      float x[3] = {ldf(p, FX, i), ldf(p, FX + 1, i), ldf(p, FX + 2, i)};
+      int b[3];
+      float f[3], w[3][3];
+      bool in_tile = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        stencil(x[a], p.inv_dx, p.res[a], b[a], f[a], w[a]);
+        in_tile &= (b[a] - tv.org[a] >= tv.lo[a]) && (b[a] - tv.org[a] <= tv.hi[a]);
+      }
+      float v[3], C[9];
+      if (in_tile)
+        g2p_gather_pk(p, tv, b, f, w, v, C);
+      else
+        g2p_gather(p, global_vel(p), b, f, w, v, C);
+      advect<SINGLE>(p, x, v);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        stf(p, FX + a, i, x[a]);
+        stf(p, FV + a, i, v[a]);
+      }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) stf(p, FC + q, i, C[q]);
+    }
+  }
+}
+
 // Exact fp64 field + contact response at one massive node inside the fp32
 // prefilter band.  Out of line: only a few percent of the nodes get here, and
 // keeping its fp64 register footprint out of grid_op_kernel lets 4 CTAs of

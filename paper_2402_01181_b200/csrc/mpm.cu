@@ -93,6 +93,8 @@ struct mpm_ctx {
   // host-converted particle transfers of pageable buffers (option
   // "host_xfer", on by default; the workers are process-wide: XferShared)
   bool host_xfer = true;
+  bool g2p_tiled = true;     // stretch-end G2P from staged velocity tiles (SOFTMPM_G2P_TILED=0: thread per particle)
+  int g2p_tile_blocks = 0;
   bool xfer_direct = true;  // with pinned buffers x / v cross as fp64 beside it (SOFTMPM_XFER_DIRECT=0: off)
   std::string err;
   long long launches = 0;
@@ -736,6 +738,24 @@ int launch_substeps(mpm_ctx* ctx, bool use_col, int row0, int nsub, bool last_cl
   return 0;
 }
 
+int launch_g2p(mpm_ctx* ctx);
+
+// The stretch-end G2P of the fast path, per work item from a staged
+// velocity tile (work list and item boxes of the stretch's last substep).
+int launch_g2p_tiled(mpm_ctx* ctx) {
+  if (!ctx->g2p_tiled) return launch_g2p(ctx);
+  TimedRegion tr(ctx, 3);
+  Params p = make_params(ctx);
+  const bool single = p.env_res[0] == p.gres[0] && p.env_res[1] == p.gres[1] && p.env_res[2] == p.gres[2] &&
+                      !p.goff[0] && !p.goff[1] && !p.goff[2];
+  if (single)
+    g2p_tile_kernel<true><<<ctx->g2p_tile_blocks, 256, sizeof(float) * 3 * TILE_NODES, ctx->stream>>>(p, ctx->item_box);
+  else
+    g2p_tile_kernel<false><<<ctx->g2p_tile_blocks, 256, sizeof(float) * 3 * TILE_NODES, ctx->stream>>>(p, ctx->item_box);
+  LAUNCHED();
+  return 0;
+}
+
 int launch_g2p(mpm_ctx* ctx) {
   TimedRegion tr(ctx, 3);
   Params p = make_params(ctx);
@@ -827,7 +847,7 @@ int run_fast_sequence(mpm_ctx* ctx, int nsub, bool col, bool skip_rebin = false)
         TRY(launch_grid_op(ctx, false, col, s + t, s + t != nsub - 1));
       }
     }
-    TRY(launch_g2p(ctx));
+    TRY(launch_g2p_tiled(ctx));
     s += L;
   }
   ctx->grid_dirty = 1;
@@ -1140,6 +1160,11 @@ int mpm_create(mpm_ctx** out, const mpm_config* cfg) {
     ctx->gsA_blocks = persistent((const void*)g2p_stress_kernel<true>, FUSED_THREADS, sizeof(float) * 6 * TILE_NODES);
     ctx->gsA0_blocks = persistent((const void*)g2p_stress_kernel<false>, FUSED_THREADS, 0);
     ctx->clear_blocks = persistent((const void*)clear_active_kernel, 256, 0);
+    ctx->g2p_tile_blocks = persistent((const void*)g2p_tile_kernel<true>, 256, sizeof(float) * 3 * TILE_NODES);
+    {
+      const char* gt = getenv("SOFTMPM_G2P_TILED");
+      if (gt) ctx->g2p_tiled = gt[0] == '1';
+    }
     ctx->fused_only_blocks = persistent((const void*)fused_kernel<true>, FUSED_K_THREADS, FUSED_SMEM);
     cudaFuncSetAttribute(substeps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(FUSED_SMEM));
